@@ -1,0 +1,179 @@
+/*
+ * rbe_cuda.h -- C ABI of the B200 exhaustive RBE retrieval path.
+ *
+ * This is the drop-in boundary: plain C types, caller-owned buffers, integer
+ * status codes.  Everything above it (the C++ rbe:: API in include/rbe/*.hpp
+ * and the Python module paper_1802_06466_b200._core) calls only these entry
+ * points; everything below it is hand-written sm_100a CUDA.
+ *
+ * Reference interfaces replaced (paths relative to the reference's proj/):
+ *   rbe_cuda_index_*          KeywordIndex / Partition held in host RAM
+ *                             (include/rbe/index.hpp:16-34) -> an HBM-resident,
+ *                             bit-plane-major device store.
+ *   rbe_cuda_search           rbe::search (include/rbe/search.hpp:68-70,
+ *                             src/search.cpp:130-168) incl. local_select
+ *                             (search.cpp:57-113), global_select
+ *                             (search.cpp:115-128) and the partition merge
+ *                             (search.cpp:160-167), batched over Q queries.
+ *   rbe_cuda_search_device    same, outputs left in device memory for the
+ *                             multi-GPU gather (replaces the std::async
+ *                             partition fan-out, search.cpp:148-157).
+ *   rbe_cuda_merge_device     the final merge under entry_less
+ *                             (search.cpp:50-53, 160-167) over gathered lists.
+ *
+ * Error model (mirrors the reference's exceptions):
+ *   RBE_CUDA_EINVAL   -> std::invalid_argument / ValueError
+ *   RBE_CUDA_ERANGE   -> std::out_of_range     / IndexError
+ *   RBE_CUDA_ERUNTIME -> std::runtime_error    / RuntimeError (CUDA, I/O)
+ * rbe_cuda_last_error() returns the thread-local message of the last failure.
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point fails with RBE_CUDA_ERUNTIME.
+ */
+#ifndef RBE_CUDA_H
+#define RBE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBE_CUDA_OK 0
+#define RBE_CUDA_EINVAL 1
+#define RBE_CUDA_ERANGE 2
+#define RBE_CUDA_ERUNTIME 3
+
+/* Scan kernel variants.  AUTO = TENSOR when the shape is supported by the
+ * tensor-core kernel, else EXACT.  Both are GPU kernels
+ * with identical results; the variant that ran is reported in
+ * rbe_search_stats.variant. */
+#define RBE_VARIANT_AUTO 0
+#define RBE_VARIANT_EXACT 1  /* CUDA-core XOR+popc, FP64 score per pair      */
+#define RBE_VARIANT_TENSOR 2 /* int8 tensor-core scan + threshold filter     */
+
+typedef struct rbe_cuda_index rbe_cuda_index;
+
+/* rbe::ScanGeometry, include/rbe/search.hpp:12-21. */
+typedef struct {
+    uint32_t blocks;
+    uint32_t threads_per_block;
+    uint32_t items_per_thread;
+    uint32_t queue_length;
+} rbe_scan_geometry;
+
+/* KeywordIndex header fields, include/rbe/index.hpp:23-27. */
+typedef struct {
+    uint32_t dim;
+    uint32_t keyword_planes;
+    uint32_t residual_weights;
+} rbe_index_shape;
+
+typedef struct {
+    uint32_t variant;      /* RBE_VARIANT_*                                       */
+    uint32_t probe_tiles;  /* TENSOR: tiles per logical block sampled for the
+                              threshold probe (0 = default)                       */
+    uint32_t reserved[6];
+} rbe_search_options;
+
+typedef struct {
+    uint64_t scored;        /* SearchStats::scored (search.hpp:45-47): Q * keywords */
+    uint32_t variant;       /* kernel that ran                                    */
+    uint32_t fallback;      /* 1 if TENSOR overflowed its candidate buffer and the
+                               batch was re-run with EXACT                        */
+    uint64_t candidates;    /* TENSOR: pairs that passed the threshold filter     */
+    uint64_t survivors;     /* per-logical-thread survivors fed to selection      */
+    double scan_ms;         /* device time of the scan kernel(s)                  */
+    double total_ms;        /* device time of the whole batch                     */
+    uint32_t launches;      /* kernels launched for the batch                     */
+    uint32_t reserved[3];
+} rbe_search_stats;
+
+/* Create an empty device index on CUDA device `device` holding
+ * `n_partitions` partitions whose global ordinals (the `partition` field of
+ * results, search.hpp:34-38) are `ordinals[i]` and sizes `counts[i]`.
+ * Device memory for all partitions is reserved here. */
+int rbe_cuda_index_create(const rbe_index_shape* shape, uint32_t n_partitions, const uint32_t* ordinals,
+                          const uint64_t* counts, int device, rbe_cuda_index** out);
+
+/* Upload local partition `i` from the reference's host layout
+ * (Partition, index.hpp:16-21): planes = plane_blocks concatenated in plane
+ * order, [keyword_planes][count * words_per_plane] u64; mags f32[count];
+ * ids u64[count].  Magnitudes must be finite and > 0 (EINVAL otherwise; the
+ * reference's load_index does not validate). */
+int rbe_cuda_index_upload_partition(rbe_cuda_index* index, uint32_t i, const uint64_t* planes,
+                                    const float* mags, const uint64_t* ids);
+
+/* Fill every local partition on the device with the synthetic corpus of
+ * global doc g of n_total, bits from counter-based
+ * splitmix64(seed) in plane-major stream order, partition g % n_partitions_total,
+ * slot g / n_partitions_total, id g, magnitude float(sqrt(sum refined^2)). */
+int rbe_cuda_index_fill_synthetic(rbe_cuda_index* index, uint64_t seed, uint64_t n_total,
+                                  uint32_t n_partitions_total);
+
+/* Copy local partition `i` back in the reference's host layout (test path). */
+int rbe_cuda_index_download_partition(const rbe_cuda_index* index, uint32_t i, uint64_t* planes,
+                                      float* mags, uint64_t* ids);
+
+int rbe_cuda_index_destroy(rbe_cuda_index* index);
+
+/* Bytes of device memory held by the index, and the algorithmic bytes one
+ * scan reads per batch (plane words + f32 magnitudes). */
+int rbe_cuda_index_bytes(const rbe_cuda_index* index, uint64_t* device_bytes, uint64_t* scan_bytes);
+
+/* Batched rbe::search.  query_words: [n_queries][query_planes][words_per_plane]
+ * u64 in the reference's PackedBinaryVector layout (binary_vector.hpp:14-21).
+ * Outputs (caller-owned host buffers, n entries per query):
+ *   scores[q*n + k], ids[q*n + k], partitions[q*n + k], accs[q*n + k]
+ *   (accs = exact integer accumulator, score = ldexp(acc, -L) / mag)
+ *   counts[q] = number of valid entries for query q (<= n).
+ * Entries are ordered by (score desc, id asc) (search.cpp:50-53).  Any of
+ * accs / stats may be NULL.  Blocking; one batch in flight per index. */
+int rbe_cuda_search(rbe_cuda_index* index, const uint64_t* query_words, uint32_t n_queries,
+                    uint32_t query_planes, const rbe_scan_geometry* geometry, uint64_t n,
+                    const rbe_search_options* options, double* scores, uint64_t* ids,
+                    uint32_t* partitions, int64_t* accs, uint64_t* counts, rbe_search_stats* stats);
+
+/* Result record in device memory (32 bytes). */
+typedef struct {
+    double score;
+    uint64_t id;
+    int64_t acc;
+    uint32_t partition;
+    uint32_t valid;
+} rbe_result;
+
+/* Same search with the query batch and outputs in DEVICE memory on the
+ * index's device: out = rbe_result[n_queries][n] (invalid tail entries have
+ * valid = 0).  `stream` is a cudaStream_t (NULL = the index's own stream);
+ * the call returns after the batch completes on that stream. */
+int rbe_cuda_search_device(rbe_cuda_index* index, const uint64_t* d_query_words, uint32_t n_queries,
+                           uint32_t query_planes, const rbe_scan_geometry* geometry, uint64_t n,
+                           const rbe_search_options* options, rbe_result* d_out, void* stream,
+                           rbe_search_stats* stats);
+
+/* Merge `n_lists` result lists per query (d_in = rbe_result[n_lists][n_queries][n],
+ * device memory on `device`) into the top n per query under (score desc,
+ * id asc): d_out = rbe_result[n_queries][n]. */
+int rbe_cuda_merge_device(int device, const rbe_result* d_in, uint32_t n_lists, uint32_t n_queries,
+                          uint64_t n, rbe_result* d_out, void* stream);
+
+/* Single-process multi-GPU rbe::search: each handle (one per device) scans its
+ * partitions into a device-resident top n, the lists are copied peer-to-peer
+ * to handles[0]'s device and merged there (rbe_cuda_merge_device); host
+ * outputs as in rbe_cuda_search.  stats->scored sums over handles. */
+int rbe_cuda_search_multi(rbe_cuda_index* const* handles, uint32_t n_handles, const uint64_t* query_words,
+                          uint32_t n_queries, uint32_t query_planes, const rbe_scan_geometry* geometry, uint64_t n,
+                          const rbe_search_options* options, double* scores, uint64_t* ids, uint32_t* partitions,
+                          int64_t* accs, uint64_t* counts, rbe_search_stats* stats);
+
+const char* rbe_cuda_last_error(void);
+
+/* Library/ABI version and the compiled device architecture, for loaders. */
+const char* rbe_cuda_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RBE_CUDA_H */

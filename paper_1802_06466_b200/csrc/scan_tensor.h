@@ -1,0 +1,31 @@
+// scan_tensor.h -- the TENSOR scan variant (scan_tensor.cu): int8 tensor-core
+// scoring of every (query, doc) pair, a conservative per-query threshold from
+// a probe pass, and exact (FP64) per-logical-thread selection of the few
+// pairs that pass it.  See DESIGN.md §4.
+#pragma once
+
+#include <string>
+
+#include "../../include/rbe_cuda.h"
+#include "internal.h"
+
+namespace rbe_dev {
+
+struct TensorScanPlan {
+    uint32_t Q = 0, qp = 0;
+    uint64_t n = 0;
+    uint32_t probe_tiles = 0;
+    uint64_t max_part_count = 0;
+    uint64_t surv_cap = 0;
+    size_t query_bytes = 0, probe_bytes = 0, threshold_bytes = 0, state_bytes = 0;
+};
+
+bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, uint32_t Q, std::string* why);
+TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, uint32_t Q,
+                                const PartDesc* d_parts, uint32_t n_parts, uint64_t n, uint32_t probe_tiles);
+// returns the number of kernels launched
+uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Shape& s, const uint64_t* d_queries,
+                         void* d_qtensor, void* d_probe, void* d_thresholds, void* d_state,
+                         unsigned long long* d_candidates, cudaStream_t st);
+
+}  // namespace rbe_dev
