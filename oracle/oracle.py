@@ -378,3 +378,22 @@ def synthetic_partitions(seed, n_total, dim, kp, n_partitions, rw=True, port=Non
         mags = port.magnitudes(planes, count, dim, kp, rw)
         parts.append((planes, mags, gids.astype(np.uint64)))
     return parts
+
+
+def synthetic_prefix(seed, n_total, count, dim, kp, rw=True, port=None):
+    """The first `count` slots of the single-partition (P=1) synthetic corpus of
+    n_total docs -- a bounded sample of the bench workload for the CPU arm."""
+    port = port or Port()
+    wpp = wpp_of(dim)
+    i = np.arange(count, dtype=np.uint64)
+    planes = np.empty((kp, count, wpp), dtype=np.uint64)
+    for t in range(kp):
+        for w in range(wpp):
+            j = (np.uint64(t) * np.uint64(n_total) + i) * np.uint64(wpp) + np.uint64(w)
+            v = splitmix64_at(seed, j)
+            if w == wpp - 1:
+                v &= np.uint64(pad_mask(dim))
+            planes[t, :, w] = v
+    planes = planes.reshape(kp, count * wpp)
+    mags = port.magnitudes(planes, count, dim, kp, rw)
+    return planes, mags, i.copy()

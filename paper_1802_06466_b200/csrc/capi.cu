@@ -107,7 +107,16 @@ struct rbe_cuda_index {
     std::mutex mu;
     // per-batch scratch, grown on demand
     DevBuf queries, qperm, qtensor, surv, surv_count, counters, queue_scratch, sel_scratch, out, probe, thresholds;
-    std::vector<Result> host_out;
+    Result* host_out = nullptr;  // pinned staging for the D2H of results
+    size_t host_out_cap = 0;
+    void ensure_host_out(size_t n) {
+        if (n <= host_out_cap) return;
+        if (host_out) cudaFreeHost(host_out);
+        host_out = nullptr;
+        host_out_cap = 0;
+        RBE_CK(cudaMallocHost(&host_out, n * sizeof(Result)));
+        host_out_cap = n;
+    }
 
     ~rbe_cuda_index() {
         cudaSetDevice(device);
@@ -116,6 +125,7 @@ struct rbe_cuda_index {
             b->release();
         if (d_parts) cudaFree(d_parts);
         if (store) cudaFree(store);
+        if (host_out) cudaFreeHost(host_out);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -157,9 +167,8 @@ struct BatchResult {
 
 // Runs one batch with queries already on the device (ix->queries) and leaves
 // rbe_result[Q][n] in ix->out.  Returns stats.
-void run_batch(rbe_cuda_index* ix, uint32_t Q, uint32_t qp, const rbe_scan_geometry* g, uint64_t n,
+void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, const rbe_scan_geometry* g, uint64_t n,
                const rbe_search_options* opt, rbe_search_stats* st_out) {
-    cudaStream_t st = ix->stream;
     const Shape& s = ix->shape;
     ScanArgs a;
     a.parts = ix->d_parts;
@@ -429,17 +438,15 @@ int rbe_cuda_search_device(rbe_cuda_index* ix, const uint64_t* d_query_words, ui
         validate_search(ix, query_planes, geometry);
         if (n_queries == 0 || n == 0) return;
         if (!d_query_words || !d_out) throw InvalidArgument("rbe_cuda_search_device: null buffer");
-        cudaStream_t user = static_cast<cudaStream_t>(stream);
+        // all work is issued on the caller's stream when given (so its events
+        // bracket exactly this batch), else on the index's own stream
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ix->stream;
         const size_t qbytes = size_t(n_queries) * query_planes * ix->shape.wpp * 8;
         ix->queries.ensure(qbytes);
-        if (user) {  // order the index stream after the caller's producer work
-            RBE_CK(cudaEventRecord(ix->ev[0], user));
-            RBE_CK(cudaStreamWaitEvent(ix->stream, ix->ev[0], 0));
-        }
-        RBE_CK(cudaMemcpyAsync(ix->queries.p, d_query_words, qbytes, cudaMemcpyDeviceToDevice, ix->stream));
-        run_batch(ix, n_queries, query_planes, geometry, n, options, stats);
-        RBE_CK(cudaMemcpyAsync(d_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToDevice, ix->stream));
-        RBE_CK(cudaStreamSynchronize(ix->stream));
+        RBE_CK(cudaMemcpyAsync(ix->queries.p, d_query_words, qbytes, cudaMemcpyDeviceToDevice, st));
+        run_batch(ix, st, n_queries, query_planes, geometry, n, options, stats);
+        RBE_CK(cudaMemcpyAsync(d_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToDevice, st));
+        RBE_CK(cudaStreamSynchronize(st));
     });
 }
 
@@ -462,9 +469,9 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
         const size_t qbytes = size_t(n_queries) * query_planes * ix->shape.wpp * 8;
         ix->queries.ensure(qbytes);
         RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, ix->stream));
-        run_batch(ix, n_queries, query_planes, geometry, n, options, stats);
-        ix->host_out.resize(size_t(n_queries) * n);
-        RBE_CK(cudaMemcpyAsync(ix->host_out.data(), ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToHost,
+        run_batch(ix, ix->stream, n_queries, query_planes, geometry, n, options, stats);
+        ix->ensure_host_out(size_t(n_queries) * n);
+        RBE_CK(cudaMemcpyAsync(ix->host_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToHost,
                                ix->stream));
         RBE_CK(cudaStreamSynchronize(ix->stream));
         for (uint32_t q = 0; q < n_queries; ++q) {
