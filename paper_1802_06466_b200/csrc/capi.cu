@@ -220,8 +220,9 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
             RBE_CK(cudaEventRecord(ix->ev[2], st));
             stats.launches += 2;
         } else {
-            TensorScanPlan plan = plan_tensor_scan(s, qp, *g, Q, ix->d_parts, a.n_parts, n, probe_tiles);
-            for (auto& p : ix->parts) plan.max_part_count = std::max(plan.max_part_count, p.count);
+            std::vector<uint64_t> counts;
+            for (auto& p : ix->parts) counts.push_back(p.count);
+            TensorScanPlan plan = plan_tensor_scan(s, qp, *g, Q, counts, n, probe_tiles);
             a.surv_cap = plan.surv_cap;
             ix->surv.ensure(sizeof(Result) * a.surv_cap * Q);
             a.surv = ix->surv.as<Result>();

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <string>
+#include <vector>
 
 #include "../../include/rbe_cuda.h"
 #include "internal.h"
@@ -15,14 +16,15 @@ struct TensorScanPlan {
     uint32_t Q = 0, qp = 0;
     uint64_t n = 0;
     uint32_t probe_tiles = 0;
-    uint64_t max_part_count = 0;
-    uint64_t surv_cap = 0;
+    uint64_t n_strips = 0;            // 128-doc strips (128 logical threads of one block)
+    std::vector<uint64_t> prefix;     // strips per local partition, cumulative [n_parts + 1]
+    uint64_t surv_cap = 0;            // per-query survivor capacity (<= 1 per logical thread)
     size_t query_bytes = 0, probe_bytes = 0, threshold_bytes = 0, state_bytes = 0;
 };
 
 bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, uint32_t Q, std::string* why);
 TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, uint32_t Q,
-                                const PartDesc* d_parts, uint32_t n_parts, uint64_t n, uint32_t probe_tiles);
+                                const std::vector<uint64_t>& counts, uint64_t n, uint32_t probe_tiles);
 // returns the number of kernels launched
 uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Shape& s, const uint64_t* d_queries,
                          void* d_qtensor, void* d_probe, void* d_thresholds, void* d_state,

@@ -203,3 +203,34 @@ def test_tensor_matches_exact_at_scale(rbe):
     b = gpu_search(rbe, dix, qs, geo, 1000, "auto")
     assert a[0] == b[0]
     assert np.array_equal(a[1], b[1])
+
+
+TENSOR_SWEEP = [
+    # N, dim, kp, qp, P, geometry, n, rw, Q
+    (20000, 64, 2, 2, 1, (1, 256, 256, 1), 100, True, 4),
+    (30000, 128, 3, 3, 1, (1, 256, 256, 1), 1000, True, 4),
+    (30000, 128, 3, 3, 3, (1, 128, 128, 1), 300, True, 3),
+    (20000, 65, 4, 2, 2, (2, 256, 64, 1), 200, True, 5),
+    (20000, 200, 1, 6, 1, (1, 384, 64, 1), 50, True, 2),
+    (20000, 100, 3, 2, 2, (1, 256, 64, 1), 100, False, 4),
+    (20000, 128, 5, 3, 1, (1, 256, 128, 1), 100, True, 3),
+    (40000, 128, 3, 3, 1, (1, 256, 256, 1), 5000, True, 2),   # n > threads: no bound, every pair rescored
+    (30000, 64, 2, 2, 1, (1, 256, 256, 1), 64, True, 70),     # two 64-query passes
+    (30000, 128, 3, 3, 1, (1, 256, 256, 1), 10, True, 1),
+]
+
+
+@pytest.mark.parametrize("case", TENSOR_SWEEP)
+def test_tensor_matches_reference(rbe, port, case):
+    N, dim, kp, qp, P, geo, n, rw, Q = case
+    ref = Ref()
+    parts = synthetic_partitions(17, N, dim, kp, P, rw, port)
+    ri = ref.index(dim, kp, rw, parts)
+    qs = gen_queries(19, Q, dim, qp)
+    want, scored = ri.search(qs, geo, n, threads=8)
+    dix = device_index(rbe, dim, kp, rw, parts)
+    got, accs, counts, stats = gpu_search(rbe, dix, qs, geo, n, "tensor")
+    assert stats["variant"] == "tensor"
+    assert stats["scored"] == scored == Q * N
+    assert got == want, case
+    check_accs(got, accs, mags_by_id(parts), qp, kp, rw)
