@@ -40,6 +40,20 @@ __host__ __device__ __forceinline__ uint32_t sel32(uint32_t m, uint32_t a, uint3
     return (a & m) | (b & ~m);  // one LOP3
 }
 
+// x >> s as a multiply-high (IMAD.HI runs on the FMA pipe, leaving the
+// half-rate ALU pipe to the LOP3 masks); s in [1, 31].
+__host__ __device__ __forceinline__ uint32_t shr(uint32_t x, int s) {
+#ifdef __CUDA_ARCH__
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - s)));
+    return r;
+#else
+    return x >> s;
+#endif
+}
+// x << s as a multiply (IMAD on the FMA pipe)
+__host__ __device__ __forceinline__ uint32_t shl(uint32_t x, int s) { return x * (1u << s); }
+
 __host__ __device__ __forceinline__ uint32_t rotr32(uint32_t x, int r) {
     return r == 0 ? x : ((x >> r) | (x << (32 - r)));
 }
@@ -60,8 +74,8 @@ struct Expand {
             uint32_t v = 0;
 #pragma unroll
             for (int t = 0; t < KP; ++t) {
-                const uint32_t b = (w[t] >> o) & 0x01010101u;
-                v += RW ? (b << (KP - 1 - t)) : b;
+                const uint32_t b = (o ? shr(w[t], o) : w[t]) & 0x01010101u;
+                v += RW ? shl(b, KP - 1 - t) : b;
             }
             out[o] = v;
         }
@@ -78,8 +92,8 @@ struct Expand<2, true> {
         const uint32_t z1 = rotr32(sel32(0x55555555u, w[0], w[1]), 1);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            out[j] = (z0 >> (2 * j)) & 0x03030303u;
-            out[4 + j] = (z1 >> (2 * j)) & 0x03030303u;
+            out[j] = (j ? shr(z0, 2 * j) : z0) & 0x03030303u;
+            out[4 + j] = (j ? shr(z1, 2 * j) : z1) & 0x03030303u;
         }
     }
 };
@@ -96,13 +110,13 @@ struct Expand<3, true> {
         const uint32_t z1 = sel32(0x49494949u, w[0], sel32(0x24242424u, w[1], w[2]));
         const uint32_t z2 = sel32(0x92929292u, w[0], sel32(0x49494949u, w[1], w[2]));
         out[0] = z0 & 0x07070707u;
-        out[1] = (z0 >> 3) & 0x07070707u;
-        out[2] = (z1 >> 1) & 0x07070707u;
-        out[3] = (z1 >> 4) & 0x07070707u;
-        out[4] = (z2 >> 2) & 0x07070707u;
-        out[5] = (z2 >> 5) & 0x07070707u;
-        out[6] = ((z0 >> 6) & 0x03030303u) | ((z1 << 2) & 0x04040404u);
-        out[7] = ((z1 >> 7) & 0x01010101u) | ((z2 << 1) & 0x06060606u);
+        out[1] = shr(z0, 3) & 0x07070707u;
+        out[2] = shr(z1, 1) & 0x07070707u;
+        out[3] = shr(z1, 4) & 0x07070707u;
+        out[4] = shr(z2, 2) & 0x07070707u;
+        out[5] = shr(z2, 5) & 0x07070707u;
+        out[6] = (shr(z0, 6) & 0x03030303u) | (shl(z1, 2) & 0x04040404u);
+        out[7] = (shr(z1, 7) & 0x01010101u) | (shl(z2, 1) & 0x06060606u);
     }
 };
 
@@ -118,7 +132,7 @@ struct Expand<4, true> {
             const uint32_t m2 = 0x11111111u << ((c + 1) & 3);
             const uint32_t z = rotr32(sel32(m0, w[0], sel32(m1, w[1], sel32(m2, w[2], w[3]))), c);
             out[2 * c] = z & 0x0F0F0F0Fu;
-            out[2 * c + 1] = (z >> 4) & 0x0F0F0F0Fu;
+            out[2 * c + 1] = shr(z, 4) & 0x0F0F0F0Fu;
         }
     }
 };
