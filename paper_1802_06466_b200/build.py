@@ -28,6 +28,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                      "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
+NVCC_FLAGS += os.environ.get("RBE_NVCC_EXTRA", "").split()  # e.g. -DRBE_PHASE_PROF (profiling builds)
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", f"-I{INCLUDE}"]
 
 CU_SOURCES = ["index_kernels.cu", "scan_exact.cu", "scan_tensor.cu", "select.cu", "capi.cu"]

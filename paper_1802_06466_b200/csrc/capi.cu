@@ -107,6 +107,8 @@ struct rbe_cuda_index {
     std::mutex mu;
     // per-batch scratch, grown on demand
     DevBuf queries, qperm, qtensor, surv, surv_count, counters, queue_scratch, sel_scratch, out, probe, thresholds;
+    bool mag_range_ok = false;   // cached magnitude range (tensor threshold bins)
+    float mag_lo = 0.0f, mag_hi = 0.0f;
     Result* host_out = nullptr;  // pinned staging for the D2H of results
     size_t host_out_cap = 0;
     void ensure_host_out(size_t n) {
@@ -193,9 +195,26 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
     ix->counters.ensure(64);
     unsigned long long* d_scored = ix->counters.as<unsigned long long>();
     unsigned int* d_overflow = reinterpret_cast<unsigned int*>(d_scored + 2);
+    unsigned int* d_error = d_overflow + 1;
     unsigned long long* d_cands = d_scored + 4;
     a.scored = d_scored;
     a.overflow = d_overflow;
+    a.error = d_error;
+    if (variant == RBE_VARIANT_TENSOR && !ix->mag_range_ok) {
+        // one-time (per index contents) magnitude range for the threshold bins
+        uint32_t* d_rng = reinterpret_cast<uint32_t*>(d_scored + 6);
+        const uint32_t init[2] = {0xffffffffu, 0u};
+        RBE_CK(cudaMemcpyAsync(d_rng, init, 8, cudaMemcpyHostToDevice, st));
+        for (auto& p : ix->parts) launch_mag_range(p.mags, p.count, d_rng, st);
+        uint32_t rng[2];
+        RBE_CK(cudaMemcpyAsync(rng, d_rng, 8, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaStreamSynchronize(st));
+        std::memcpy(&ix->mag_lo, &rng[0], 4);
+        std::memcpy(&ix->mag_hi, &rng[1], 4);
+        ix->mag_range_ok = true;
+    }
+    a.mag_lo = ix->mag_lo;
+    a.mag_hi = ix->mag_hi;
 
     RBE_CK(cudaEventRecord(ix->ev[0], st));
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -235,9 +254,11 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
                                               ix->thresholds.p, ix->queue_scratch.p, d_cands, st);
             RBE_CK(cudaEventRecord(ix->ev[2], st));
         }
-        unsigned int overflow = 0;
-        RBE_CK(cudaMemcpyAsync(&overflow, d_overflow, sizeof(overflow), cudaMemcpyDeviceToHost, st));
+        unsigned int flags[2] = {0, 0};
+        RBE_CK(cudaMemcpyAsync(flags, d_overflow, sizeof(flags), cudaMemcpyDeviceToHost, st));
         RBE_CK(cudaStreamSynchronize(st));
+        if (flags[1]) throw std::logic_error("tensor scan: accumulator recovery failed (internal error)");
+        const unsigned int overflow = flags[0];
         if (!overflow) break;
         if (variant == RBE_VARIANT_EXACT) throw std::logic_error("exact scan overflowed its survivor list");
         // candidate/survivor buffer overflow in the tensor kernel: redo exactly.
@@ -362,6 +383,7 @@ int rbe_cuda_index_upload_partition(rbe_cuda_index* ix, uint32_t i, const uint64
         tmp.ensure(nat_bytes + 64);
         RBE_CK(cudaMemcpyAsync(tmp.p, planes, nat_bytes, cudaMemcpyHostToDevice, ix->stream));
         launch_repack_planes(tmp.as<uint64_t>(), L.planes, L.count, L.count_pad, s, ix->perm, ix->stream);
+        ix->mag_range_ok = false;
         RBE_CK(cudaMemcpyAsync(L.mags, mags, L.count * 4, cudaMemcpyHostToDevice, ix->stream));
         RBE_CK(cudaMemcpyAsync(L.ids, ids, L.count * 8, cudaMemcpyHostToDevice, ix->stream));
         ix->counters.ensure(64);
@@ -381,6 +403,7 @@ int rbe_cuda_index_fill_synthetic(rbe_cuda_index* ix, uint64_t seed, uint64_t n_
         std::lock_guard<std::mutex> lk(ix->mu);
         DeviceGuard dg(ix->device);
         if (n_parts_total == 0) throw InvalidArgument("rbe_cuda_index_fill_synthetic: need at least one partition");
+        ix->mag_range_ok = false;
         for (auto& L : ix->parts) {
             if (L.ordinal >= n_parts_total) throw InvalidArgument("rbe_cuda_index_fill_synthetic: ordinal >= partitions");
             const uint64_t expect = L.ordinal < n_total ? (n_total - L.ordinal + n_parts_total - 1) / n_parts_total : 0;

@@ -145,6 +145,25 @@ __global__ void validate_mags_kernel(const float* __restrict__ mags, uint64_t co
     }
 }
 
+// min / max of positive finite magnitudes as order-preserving u32 bit patterns
+__global__ void mag_range_kernel(const float* __restrict__ mags, uint64_t count, uint32_t* out) {
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < count;
+         s += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t b = __float_as_uint(mags[s]);
+        lo = min(lo, b);
+        hi = max(hi, b);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, lo);
+        atomicMax(out + 1, hi);
+    }
+}
+
 __global__ void fill_f32_kernel(float* p, uint64_t n, float v) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
         p[i] = v;
@@ -181,6 +200,12 @@ void launch_fill_synthetic(uint32_t* d_planes, float* d_mags, uint64_t* d_ids, u
 void launch_validate_mags(const float* d_mags, uint64_t count, uint32_t* d_bad, cudaStream_t st) {
     if (count == 0) return;
     validate_mags_kernel<<<grid_for(count), kThreads, 0, st>>>(d_mags, count, d_bad);
+    RBE_CK(cudaGetLastError());
+}
+
+void launch_mag_range(const float* d_mags, uint64_t count, uint32_t* d_out, cudaStream_t st) {
+    if (count == 0) return;
+    mag_range_kernel<<<grid_for(count), kThreads, 0, st>>>(d_mags, count, d_out);
     RBE_CK(cudaGetLastError());
 }
 

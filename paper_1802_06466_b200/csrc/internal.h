@@ -51,6 +51,8 @@ void launch_fill_synthetic(uint32_t* d_planes, float* d_mags, uint64_t* d_ids, u
                            uint64_t seed, const Shape& s, const PlanePerm& perm, cudaStream_t st);
 void launch_validate_mags(const float* d_mags, uint64_t count, uint32_t* d_bad, cudaStream_t st);
 void launch_fill_f32(float* p, uint64_t n, float v, cudaStream_t st);
+// d_out[0] = min, d_out[1] = max magnitude bits (caller initialises to ~0u / 0)
+void launch_mag_range(const float* d_mags, uint64_t count, uint32_t* d_out, cudaStream_t st);
 
 // ---- per-batch query preparation (scan_exact.cu)
 // natural query words [Q][qp][wpp] u64 -> permuted u32 words for the exact
@@ -69,6 +71,8 @@ struct ScanArgs {
     uint64_t surv_cap = 0;
     unsigned long long* scored = nullptr;      // [1]
     unsigned int* overflow = nullptr;          // [1]
+    unsigned int* error = nullptr;             // [1] internal consistency failures (tensor scan)
+    float mag_lo = 0.0f, mag_hi = 0.0f;        // magnitude range of the index (tensor threshold bins)
 };
 
 // ---- exact kernel (scan_exact.cu)

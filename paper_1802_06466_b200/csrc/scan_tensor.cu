@@ -14,8 +14,20 @@
 // so acc = D + C_q with D = (s8 query bytes) x (u8 doc bytes) on the tensor
 // cores (tcgen05.mma kind::i8, s32 accumulators in TMEM) and C_q a per-query
 // constant.  The doc bytes V_j are produced from the bit-plane-major store by
-// the expand32 bit tricks (rbe_common.cuh) straight into TMEM (tcgen05.st),
+// the Expand bit tricks (rbe_common.cuh) straight into TMEM (tcgen05.st),
 // which is the MMA's A operand.
+//
+// Threshold folded into the MMA.  The query operand carries sigma * rq
+// (sigma = 2 lambda, a power of two) in the data K blocks plus one extra
+// 32-byte K block X whose doc-side bytes are [j, j, j, j, j>>4, 1, 0, 0,
+// 255 x 24] with j = the doc's magnitude bin (m >= m0 + Delta j).  The
+// tensor core therefore produces, per pair,
+//     F = lambda (acc - C_q) + X_q(j),   X_q(j) = c_q - e_q j - g_q (j >> 4),
+// with (c, e, g) chosen from the query's current score threshold theta_q so
+// that  score >= theta_q  implies  F >= 0  (x_coeffs below; every rounding is
+// conservative).  The epilogue only ANDs the 64 accumulators of a doc and
+// tests one sign bit; the rare passing pairs recover acc exactly from F and
+// are scored in FP64 (IEEE division, bit-identical to the CPU reference).
 //
 // Selection.  Algorithm 1 keeps, per logical thread (x, y), its best
 // queue_length(=1) items (search.cpp:32-48, 57-113); only the top n survivors
@@ -23,71 +35,77 @@
 // `probe_tiles` tiles of every logical block gives, per query, the n-th largest
 // of per-thread maxima over distinct threads -- a lower bound theta_q on the
 // final n-th survivor score.  Items scoring below theta_q can neither be in
-// the top n nor change which items >= theta_q survive, so the main pass keeps
-// a per-(query, thread) queue only for the pairs that pass an integer
-// threshold test on D (one ISETP per pair); those few are scored exactly in
-// FP64 (IEEE division, bit-identical to the CPU) and ranked with the
-// reference's tie rules.  Scores of all other pairs never leave the SM.
+// the top n nor change which items >= theta_q survive.  theta_q is raised at
+// every strip end from a global histogram of emitted survivors (each a final
+// per-thread best of a distinct logical thread), and the X block of the
+// query operand is rewritten in shared memory.
 //
 // Kernel anatomy (one CTA per SM, persistent over 128-doc "strips" = the
 // 128 logical threads y in [128h, 128h+128) of logical block x):
-//   warp 8        producer: cp.async.bulk of each sub-tile's plane words into
-//                 a shared-memory ring (mbarrier complete_tx); TMEM allocator
-//   warp 9        MMA issuer: tcgen05.mma.cta_group::1.kind::i8, A (docs) from
-//                 TMEM, B (queries) from shared memory, D double-buffered
-//   warps 0-3     expanders: bit planes -> u8 V bytes -> tcgen05.st into A
-//   warps 4-7     epilogue: tcgen05.ld of D, threshold filter, exact FP64
-//                 rescoring + per-thread queue in shared memory, survivor
-//                 emission at strip end
+//   warp 4*nwg    producer: cp.async.bulk of each sub-tile's plane words and
+//                 magnitudes into a shared-memory ring (mbarrier complete_tx);
+//                 TMEM allocator
+//   warpgroups    nwg (2..4) workers; warpgroup w takes sub-tiles u = w (mod
+//                 nwg): expand bit planes -> u8 V bytes -> tcgen05.st into its
+//                 A; its leader issues the MMAs (A from TMEM, B = queries from
+//                 shared memory) into its D; the warpgroup then tests D.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "scan_tensor.h"
 
 namespace rbe_dev {
 namespace {
 
-constexpr int kStages = 6;           // ring of 128-doc sub-tiles
-constexpr int kWG = 3;               // worker warpgroups (expand -> MMA -> filter each)
-constexpr int kWorkerWarps = 4 * kWG;
-constexpr int kWorkers = 32 * kWorkerWarps;
-constexpr int kProducerWarp = kWorkerWarps;
-constexpr int kThreads = kWorkers + 32;
-constexpr int kAllBar = 8;           // named barrier of all worker threads (1..kWG: per warpgroup)
-constexpr int kQPass = 64;           // queries per pass (state is [64][128] in shared memory)
-constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr int kStages = 12;          // ring of 128-doc sub-tiles
+constexpr int kMaxWG = 3;            // worker warpgroups (13 warps: <= 4 per SMSP -> 128 registers)
+constexpr int kMaxThreads = 32 * (5 * kMaxWG + 1);  // workers + producer + MMA issuers
+constexpr uint32_t kCandQueue = 512;  // deferred candidates per strip (shared memory; overflow is scored at once)
+constexpr int kAllBar = 8;           // named barrier of all worker threads (1..nwg: per warpgroup)
+constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
 constexpr unsigned long long kEmptyKey = ~0ull;
-constexpr int kProbeTop = 4;         // per-(query, strip) values kept by the probe
-constexpr uint32_t kList = 6;        // deferred FP64 candidates per worker thread
 constexpr int kBins = 64;            // dynamic-theta histogram bins per query
+constexpr int kHiCols = 24;          // X block: K bytes 8..31 hold 255 (the c_q "high" part)
+constexpr int32_t kXMax = 255 * kHiCols * 127 + 127;  // largest |X| the block can encode
+constexpr int32_t kEMax = 4 * 127;   // e_q is split over 4 K bytes
 
 struct TensorParams {
     const PartDesc* parts;
     const uint64_t* strip_prefix;  // [n_parts + 1] cumulative strip counts
     uint32_t n_parts;
     uint32_t tpb, ipt;
-    uint32_t w32;                  // u32 words per doc plane
+    uint32_t w32;                  // u32 words per doc plane (= data K blocks)
+    uint32_t nwg;                  // worker warpgroups
+    uint32_t nstages;              // ring depth (stages of sw docs)
+    uint32_t sw;                   // strip width in logical threads (128 or 256) = docs per stage
+    uint32_t ptop;                 // probe: values kept per (query, strip)
     uint32_t q0, nq;               // query range of this pass
     uint32_t n_pad;                // MMA N (multiple of 16, >= nq)
     uint32_t L;                    // 2^-L scale (qp + kp - 2, or 0 unweighted)
-    const uint8_t* bimg;           // [nq_total][...] pre-laid-out B image for this pass
+    uint32_t lam_shift;            // lambda = 2^lam_shift (query operand = 2 lambda rq)
+    float m0f, inv_df;             // magnitude bins: j = floor((m - m0) / Delta)
+    double m0, delta, mmax;
+    const uint8_t* bimg;           // pre-laid-out B image (data K blocks) for this pass
     const int32_t* cq;             // [Q] query constants
     const double* theta;           // [Q] exact-score threshold (main pass)
-    const double* t2l;             // [Q] theta * 2^L (main pass)
     uint32_t probe_tiles;          // probe pass: tiles per strip (0 = main pass)
-    float* probe_out;              // [Q][n_strips * kProbeTop]
+    float* probe_out;              // [Q][n_strips][ptop]
     uint64_t n_strips;
     Result* surv;
     unsigned long long* surv_count;
     uint64_t surv_cap;
     unsigned long long* scored;
     unsigned long long* candidates;
+    unsigned int* error;
     uint32_t* hist;                // [Q][kBins] emitted-survivor histogram (dynamic theta)
-    const double* delta;           // [Q] histogram bin width (score units)
+    const double* delta_h;         // [Q] histogram bin width (score units)
     const double* theta0;          // [Q] probe theta (bin 0 lower edge)
     uint64_t n;                    // top-n
+    unsigned long long* prof;      // optional [grid][kMaxWG][8] phase cycle counters (RBE_PROF=1)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -118,6 +136,20 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try(bar, parity)) {
     }
+}
+// waits on the tensor core: let the hardware suspend the warp until the phase
+// completes (or the hint expires) instead of re-polling
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000u)
+            : "memory");
+    } while (!ok);
 }
 // long waits (the producer on a full ring): back off so the spinning warp does
 // not steal issue slots from the working ones
@@ -172,6 +204,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t* v) {
         : "r"(taddr)
         : "memory");
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr)
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -211,47 +249,102 @@ __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N) {
     return (2u << 4) | (0u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t a, uint32_t b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
+}
+
 struct StripInfo {
     uint32_t part;
-    uint64_t x, h;
-    uint32_t n_tiles;
+    uint64_t base;     // first slot of the strip: x * tpb * ipt + hs * sw
+    uint32_t n_tiles;  // tiles (stages of sw contiguous docs) of the strip
 };
 
+// Strip s = logical threads [hs*sw, hs*sw + sw) of logical block x of a partition
+// (thread_assignment, search.cpp:10-26): its tile i is the sw contiguous slots
+// x*tpb*ipt + i*tpb + hs*sw + [0, sw).
 __device__ __forceinline__ StripInfo strip_info(const TensorParams& p, uint64_t s) {
-    StripInfo si{0, 0, 0, 0};
+    StripInfo si{0, 0, 0};
     uint32_t part = 0;
     while (part + 1 < p.n_parts && p.strip_prefix[part + 1] <= s) ++part;
     const uint64_t local = s - p.strip_prefix[part];
-    const uint32_t spb = p.tpb / 128;
+    const uint32_t spb = p.tpb / p.sw;
+    const uint64_t x = local / spb, hs = local % spb;
     si.part = part;
-    si.x = local / spb;
-    si.h = local % spb;
+    si.base = x * uint64_t(p.tpb) * p.ipt + p.sw * hs;
     const uint64_t count = p.parts[part].count;
-    const uint64_t base = si.x * uint64_t(p.tpb) * p.ipt + 128 * si.h;
     uint64_t nt = 0;
-    if (count > base) nt = (count - base + p.tpb - 1) / p.tpb;
+    if (count > si.base) nt = (count - si.base + p.tpb - 1) / p.tpb;
     if (nt > p.ipt) nt = p.ipt;
     if (p.probe_tiles && nt > p.probe_tiles) nt = p.probe_tiles;
     si.n_tiles = uint32_t(nt);
     return si;
 }
 
+// ------------------------------------------------------------ threshold block
+struct XCoef {
+    int32_t c, e, g;  // X(j) = c - e j - g (j >> 4)
+};
 
-// Stage-1 filter coefficients for query q from t = theta * 2^L (rounded
-// down): D >= floor(ta * m + tc) is necessary for score >= theta, where m is
-// the minimum (t >= 0) or maximum (t < 0) magnitude of the docs tested.
-// No bound (t = -inf) -> everything passes; dead column (t = +inf) -> nothing.
-__device__ __forceinline__ void set_filter_coeffs(float t, int32_t cq, float* ta, float* tc) {
-    if (!(t > -INFINITY)) {
-        *ta = 0.0f;
-        *tc = -3.0e9f;
-    } else if (t == INFINITY) {
-        *ta = 0.0f;
-        *tc = 3.0e9f;
+// Coefficients of the X block for a query with exact-score threshold theta:
+// score >= theta  =>  F = lambda (acc - C_q) + X(j) >= 0 for every doc whose
+// magnitude bin is j (m0 + Delta j <= m <= mmax).  score = RN(acc 2^-L / m)
+// >= theta implies acc >= t m with t = theta 2^L lowered by 2^-40 relative;
+// then X(j) >= lambda (C_q - t m) is required:
+//   t >= 0:  lambda (C - t m) <= lambda (C - t m0) - beta j, beta = lambda t Delta,
+//            c = ceil(lambda (C - t m0) + margin), e + g/16 <= beta (floors)
+//   t <  0:  lambda (C - t m) <= lambda (C - t mmax) = c, e = g = 0.
+// Out-of-range values clamp in the conservative direction (larger X).
+__device__ XCoef x_coeffs(double theta, int32_t Cq, int L, double lam, double m0, double delta, double mmax) {
+    if (!(theta > -INFINITY)) return XCoef{kXMax, 0, 0};  // no bound: every pair passes
+    if (theta == INFINITY) return XCoef{-kXMax, 0, 0};    // dead query: no pair passes
+    const double t = ldexp(theta, L);
+    double c;
+    int32_t e = 0, g = 0;
+    if (t >= 0.0) {
+        const double tl = t * (1.0 - 0x1p-40);
+        c = lam * (double(Cq) - tl * m0);
+        double beta = lam * tl * delta * (1.0 - 0x1p-40);
+        if (beta > double(kEMax)) beta = double(kEMax);
+        const double ef = floor(beta);
+        e = int32_t(ef);
+        g = int32_t(floor((beta - ef) * 16.0 * (1.0 - 0x1p-30)));
+        g = g < 0 ? 0 : (g > 15 ? 15 : g);
     } else {
-        *ta = t >= 0.0f ? __fmul_rd(t, 0.99999f) : __fmul_rd(t, 1.00001f);
-        *tc = __fadd_rd(-float(cq), -2.0f);
+        const double tl = t * (1.0 + 0x1p-40);
+        c = lam * (double(Cq) - tl * mmax);
     }
+    c = ceil(c + fabs(c) * 0x1p-40 + 1.0);
+    if (!(c < double(kXMax))) return XCoef{kXMax, 0, 0};
+    if (c < -double(kXMax)) c = -double(kXMax);
+    return XCoef{int32_t(c), e, g};
+}
+
+// Row r of the X K block (block index kd) of the B image: s8 bytes
+// [-e0..-e3, -g, lo, 0, 0, h0..h23], c = 255 sum(h) + lo, e = sum(e_i).
+__device__ void write_xrow(uint8_t* bsm, uint32_t n_pad, uint32_t kd, uint32_t r, const XCoef& x) {
+    uint8_t* base = bsm + size_t(kd) * n_pad * 32 + (r / 8) * 256 + (r % 8) * 16;
+    auto put = [&](int k, int v) { base[(k / 16) * 128 + (k % 16)] = uint8_t(int8_t(v)); };
+    const int32_t H = x.c >= 0 ? (x.c + 127) / 255 : -((-x.c + 127) / 255);
+    const int32_t lo = x.c - 255 * H;
+    for (int i = 0; i < 4; ++i) put(i, -(x.e / 4 + (i < x.e % 4 ? 1 : 0)));
+    put(4, -x.g);
+    put(5, lo);
+    put(6, 0);
+    put(7, 0);
+    const int32_t hb = H / kHiCols, hr = H - kHiCols * hb;  // hr has the sign of H
+    for (int i = 0; i < kHiCols; ++i) {
+        int v = hb;
+        if (i < (hr >= 0 ? hr : -hr)) v += hr >= 0 ? 1 : -1;
+        put(8 + i, v);
+    }
+}
+
+// magnitude bin: floor((m - m0) / Delta) lowered by 1e-3 so that m0 + Delta j <= m
+// holds in real arithmetic despite the float rounding; clamped to [0, 255]
+__device__ __forceinline__ uint32_t mag_bin(float m, float m0, float inv_d) {
+    float v = __fmaf_rz(m - m0, inv_d, -1.0e-3f);
+    v = fminf(fmaxf(v, 0.0f), 255.0f);
+    return uint32_t(__float2int_rz(v));
 }
 
 // position in a ring of n slots + the parity of the current pass over it
@@ -266,90 +359,145 @@ struct RingPos {
 };
 
 struct SmemLayout {
-    size_t b, state, lists, thr, qconst, bars, total;
+    size_t b, state, cqueue, qconst, bars, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uint32_t n_pad, bool probe) {
+__host__ __device__ inline size_t stage_bytes_of(uint32_t kp, uint32_t w32, uint32_t sw) {
+    return size_t(sw) * (size_t(kp) * w32 * 4 + 4);
+}
+
+__host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uint32_t n_pad, uint32_t nstages,
+                                                  uint32_t sw, bool probe) {
     auto al = [](size_t x) { return (x + 127) & ~size_t(127); };
     SmemLayout s{};
-    size_t off = al(size_t(kStages) * (kp * 128 * w32 * 4 + 512));
+    size_t off = al(size_t(nstages) * stage_bytes_of(kp, w32, sw));
     s.b = off;
-    off = al(off + size_t(n_pad) * 32 * w32);
+    off = al(off + size_t(n_pad) * 32 * (w32 + 1));
     s.state = off;
-    off = al(off + (probe ? size_t(kQPass) * 128 * 4 : size_t(kQPass) * 128 * 8));
-    s.lists = off;
-    off = al(off + (probe ? 0 : size_t(kWorkers) * kList * 12));
-    s.thr = off;
-    off = al(off + size_t(kWorkerWarps) * kQPass * 4 + kQPass * 4);
+    off = al(off + size_t(kQPass) * sw * (probe ? 4 : 8));
+    s.cqueue = off;
+    off = al(off + (probe ? 0 : size_t(kCandQueue) * 8));
     s.qconst = off;
-    off = al(off + kQPass * 8 + kQPass * 4 * 3);
+    off = al(off + kQPass * 8 + kQPass * 4 * 4);
     s.bars = off;
-    off = al(off + (kStages * 2 + kWG) * 8 + 16);
+    off = al(off + (2 * nstages + 2 * kMaxWG) * 8 + 16);
     s.total = off;
     return s;
 }
 
+// One passing pair (F >= 0): recover acc exactly, score it in FP64 and merge it
+// into the per-(query, logical thread) state under (score desc, slot asc)
+// (BoundedQueue::insert, search.cpp:32-48).  Entries hold key = (i << 32 | acc);
+// the order is independent of insertion order, so warpgroups may update the
+// same entry concurrently (64-bit CAS).
+__device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, uint32_t i, uint32_t col, uint32_t sw,
+                                            const double* theta_s, unsigned long long* st_key, const float* mags_y,
+                                            uint32_t tpb, int L) {
+    const double sc = __ddiv_rn(ldexp(double(a), -L), double(mag));
+    if (!(sc >= theta_s[q])) return;
+    const unsigned long long mine = (uint64_t(i) << 32) | uint32_t(a);
+    unsigned long long* ent = st_key + q * sw + col;
+    unsigned long long cur = *ent;
+    while (true) {
+        if (cur != kEmptyKey) {
+            const uint32_t ci = uint32_t(cur >> 32);
+            const double cm = double(__ldg(mags_y + uint64_t(ci) * tpb));
+            const double cs = __ddiv_rn(ldexp(double(int32_t(uint32_t(cur))), -L), cm);
+            if (!(sc > cs || (sc == cs && i < ci))) break;  // the current entry ranks first
+        }
+        const unsigned long long prev = atomicCAS(ent, cur, mine);
+        if (prev == cur) break;
+        cur = prev;
+    }
+}
+
+// phase timing of the worker loop (build with -DRBE_PHASE_PROF and run with RBE_PROF=1)
+#ifdef RBE_PHASE_PROF
+#define RBE_CLK(x) const long long x = clock64()
+#define RBE_CLK_DECL(x) long long x = 0
+#define RBE_CLK_SET(x) x = clock64()
+#define RBE_CLK_COPY(x, y) x = y
+#else
+#define RBE_CLK(x)
+#define RBE_CLK_DECL(x)
+#define RBE_CLK_SET(x)
+#define RBE_CLK_COPY(x, y)
+#endif
+
 template <int KP, bool RW, bool PROBE>
-__global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p) {
+__global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t w32 = p.w32;
-    const uint32_t plane_bytes = 128 * w32 * 4;          // one plane of a 128-doc sub-tile
-    const uint32_t stage_bytes = KP * plane_bytes + 512; // + the sub-tile's f32 magnitudes
-    const uint32_t kbytes = 32 * w32;                    // K bytes per row (u8 per bit position)
-    const uint32_t n_kb = w32;                           // one 32-byte K block per 32-dim group
-    SmemLayout sl = smem_layout(KP, w32, p.n_pad, PROBE);
+    const uint32_t nwg = p.nwg;
+    const uint32_t n_workers = 128 * nwg;
+    const uint32_t nst = p.nstages;
+    const uint32_t sw = p.sw;                              // strip width (logical threads): 128 or 256
+    const uint32_t spt = sw / 128;                         // 128-doc sub-tiles per stage
+    const uint32_t plane_bytes = sw * w32 * 4;             // one plane of a stage (sw docs)
+    const uint32_t stage_bytes = KP * plane_bytes + sw * 4;  // + the stage's f32 magnitudes
+    const uint32_t n_kb = w32 + 1;                         // data K blocks + the X block
+    SmemLayout sl = smem_layout(KP, w32, p.n_pad, nst, sw, PROBE);
     uint8_t* ring = smem;
     uint8_t* bsm = smem + sl.b;
-    unsigned long long* st_key = reinterpret_cast<unsigned long long*>(smem + sl.state);  // [64][128]
-    float* pmax = reinterpret_cast<float*>(smem + sl.state);                              // probe: [64][128]
-    uint32_t* ls_qi = reinterpret_cast<uint32_t*>(smem + sl.lists);  // [kList][kWorkers]
-    int32_t* ls_acc = reinterpret_cast<int32_t*>(ls_qi + kWorkers * kList);
-    float* ls_mag = reinterpret_cast<float*>(ls_acc + kWorkers * kList);
-    int32_t* T_w = reinterpret_cast<int32_t*>(smem + sl.thr);        // [kWorkerWarps][64]
-    int32_t* cq_s = T_w + kWorkerWarps * kQPass;                      // [64]
-    double* theta_s = reinterpret_cast<double*>(smem + sl.qconst);   // [64]
-    float* t2l_s = reinterpret_cast<float*>(theta_s + kQPass);       // [64]
-    float* ta_s = t2l_s + kQPass;                                     // [64] threshold slope
-    float* tc_s = ta_s + kQPass;                                      // [64] threshold offset
+    unsigned long long* st_key = reinterpret_cast<unsigned long long*>(smem + sl.state);  // [64][sw]
+    float* pmax = reinterpret_cast<float*>(smem + sl.state);                              // probe: [64][sw]
+    uint2* cqueue = reinterpret_cast<uint2*>(smem + sl.cqueue);     // deferred candidates
+    double* theta_s = reinterpret_cast<double*>(smem + sl.qconst);  // [64]
+    int32_t* cq_s = reinterpret_cast<int32_t*>(theta_s + kQPass);   // [64]
+    int32_t* xc_s = cq_s + kQPass;                                  // [64] X coefficients
+    int32_t* xe_s = xc_s + kQPass;
+    int32_t* xg_s = xe_s + kQPass;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sl.bars);
-    uint64_t* full = bars;
-    uint64_t* empty = full + kStages;
-    uint64_t* mma_done = empty + kStages;  // [kWG]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + kWG);
+    uint64_t* full = bars;                 // [nst]  ring slot loaded (tx bytes)
+    uint64_t* empty = full + nst;          // [nst]  ring slot consumed (128 arrivals per sub-tile)
+    uint64_t* a_full = empty + nst;        // [nwg]  A complete and D free (4 warp arrivals)
+    uint64_t* mma_done = a_full + kMaxWG;  // [nwg]  MMA committed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + kMaxWG);
+    uint32_t* cq_count = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t a_cols = 8 * w32;   // TMEM columns of one sub-tile's A
+    const int producer_warp = int(4 * nwg);
+    const int mma_warp0 = producer_warp + 1;  // nwg MMA issuer warps follow the producer
+    const uint32_t a_cols = 8 * n_kb;  // TMEM columns of one sub-tile's A (4 K bytes per column)
     const uint32_t d_cols = p.n_pad;   // TMEM columns of one sub-tile's D
     uint32_t tmem_cols = 32;
-    while (tmem_cols < kWG * (a_cols + d_cols)) tmem_cols <<= 1;
+    while (tmem_cols < nwg * (2 * a_cols + d_cols)) tmem_cols <<= 1;
     const int L = int(p.L);
+    const double lam = double(1u << p.lam_shift);
 
-    // ---- one-time setup
-    for (uint32_t e = threadIdx.x; e < p.n_pad * kbytes / 16; e += blockDim.x)
+    // ---- one-time setup: B image (data blocks from global, X block per query)
+    for (uint32_t e = threadIdx.x; e < p.n_pad * 32 * w32 / 16; e += blockDim.x)
         reinterpret_cast<uint4*>(bsm)[e] = reinterpret_cast<const uint4*>(p.bimg)[e];
     for (uint32_t q = threadIdx.x; q < kQPass; q += blockDim.x) {
         const bool live = q < p.nq;
         cq_s[q] = live ? p.cq[p.q0 + q] : 0;
         theta_s[q] = (live && !PROBE) ? p.theta[p.q0 + q] : INFINITY;
-        // float copy of theta*2^L rounded toward -inf (a conservative filter value)
-        const double t = (live && !PROBE) ? p.t2l[p.q0 + q] : INFINITY;
-        t2l_s[q] = __double2float_rd(t);
-        set_filter_coeffs(t2l_s[q], cq_s[q], ta_s + q, tc_s + q);
+        XCoef x;
+        if (PROBE) x = live ? XCoef{int32_t(cq_s[q] * int32_t(1u << p.lam_shift)), 0, 0} : XCoef{-kXMax, 0, 0};
+        else x = x_coeffs(theta_s[q], cq_s[q], L, lam, p.m0, p.delta, p.mmax);
+        xc_s[q] = x.c;
+        xe_s[q] = x.e;
+        xg_s[q] = x.g;
+        write_xrow(bsm, p.n_pad, w32, q, x);
     }
-    for (uint32_t e = threadIdx.x; e < kQPass * 128; e += blockDim.x) {
+    for (uint32_t e = threadIdx.x; e < kQPass * sw; e += blockDim.x) {
         if (PROBE) pmax[e] = -INFINITY;
         else st_key[e] = kEmptyKey;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (uint32_t s = 0; s < nst; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 128);
+            mbar_init(empty + s, 128 * spt);
         }
-        for (int w = 0; w < kWG; ++w) mbar_init(mma_done + w, 1);
+        for (uint32_t w = 0; w < nwg; ++w) {
+            mbar_init(a_full + w, 4);
+            mbar_init(mma_done + w, 1);
+        }
+        *cq_count = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == kProducerWarp) {
+    if (warp == producer_warp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -361,99 +509,129 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == kProducerWarp) {
-        // ===================== producer: bulk copies of sub-tiles into the ring =====================
+    if (warp == producer_warp) {
+        // ===================== producer: one contiguous sw-doc stage per tile of the strip =====================
         if (lane == 0) {
             RingPos rs;
+#ifdef RBE_PHASE_PROF
+            long long t_wait = 0, t_start = clock64();
+#endif
             for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
                 const StripInfo si = strip_info(p, s);
                 const PartDesc& part = p.parts[si.part];
-                for (uint32_t i = 0; i < si.n_tiles; ++i, rs.next(kStages)) {
-                    mbar_wait_backoff(empty + rs.idx, rs.phase ^ 1);
+                for (uint32_t i = 0; i < si.n_tiles; ++i, rs.next(nst)) {
+#ifdef RBE_PHASE_PROF
+                    const long long tw = clock64();
+#endif
+                    mbar_wait_sleep(empty + rs.idx, rs.phase ^ 1);
+#ifdef RBE_PHASE_PROF
+                    t_wait += clock64() - tw;
+#endif
                     mbar_expect_tx(full + rs.idx, stage_bytes);
-                    const uint64_t slot0 = si.x * uint64_t(p.tpb) * p.ipt + uint64_t(i) * p.tpb + 128 * si.h;
+                    const uint64_t slot0 = si.base + uint64_t(i) * p.tpb;
                     uint8_t* dst = ring + rs.idx * stage_bytes;
 #pragma unroll
                     for (int t = 0; t < KP; ++t)
                         bulk_g2s(dst + t * plane_bytes, part.planes + (uint64_t(t) * part.count_pad + slot0) * w32,
                                  plane_bytes, full + rs.idx);
-                    bulk_g2s(dst + KP * plane_bytes, part.mags + slot0, 512, full + rs.idx);
+                    bulk_g2s(dst + KP * plane_bytes, part.mags + slot0, sw * 4, full + rs.idx);
+                }
+            }
+#ifdef RBE_PHASE_PROF
+            if (p.prof) {
+                p.prof[(uint64_t(blockIdx.x) * kMaxWG) * 8 + 6] += t_wait;
+                p.prof[(uint64_t(blockIdx.x) * kMaxWG) * 8 + 7] += clock64() - t_start;
+            }
+#endif
+        }
+    } else if (warp >= mma_warp0 && warp < mma_warp0 + int(nwg)) {
+        // ===================== MMA issuers: one warp per warpgroup, its sub-tiles in order =====================
+        const uint32_t w = uint32_t(warp - mma_warp0);
+        if (lane == 0) {
+            const uint32_t idesc = idesc_i8(128, p.n_pad);
+            const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
+            const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
+            const uint32_t a_base = tmem_base + w * (2 * a_cols + d_cols);
+            const uint32_t d_t = a_base + 2 * a_cols;
+            uint32_t c = 0, u0 = 0;
+            for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
+                const StripInfo si = strip_info(p, s);
+                const uint32_t n_sub = si.n_tiles * spt;
+                // this warpgroup's sub-tiles of the strip: k = first, first + nwg, ...
+                const uint32_t first = (w + nwg - u0 % nwg) % nwg;
+                const uint32_t mine = n_sub > first ? (n_sub - first + nwg - 1) / nwg : 0;
+                u0 += n_sub;
+                for (uint32_t k = 0; k < mine; ++k, ++c) {
+                    mbar_wait_sleep(a_full + w, c & 1);
+                    tc_fence_after();
+                    const uint32_t a_t = a_base + (c & 1) * a_cols;
+                    uint64_t bd = b_desc0;
+                    for (uint32_t kb = 0; kb < n_kb; ++kb, bd += b_step) mma_i8(d_t, a_t + 8 * kb, bd, idesc, kb > 0);
+                    mma_commit(mma_done + w);
                 }
             }
         }
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
-        return;
-    }
-
-    // ===================== workers: warpgroup wg handles sub-tiles u = wg (mod kWG) =====================
-    const uint32_t wg = uint32_t(warp >> 2);
-    const int quad = warp & 3;
-    const uint32_t l = uint32_t(quad * 32 + lane);        // TMEM lane == doc within the sub-tile
-    const uint32_t wt = uint32_t(threadIdx.x);            // worker thread id (list owner)
-    const uint32_t lane_base = uint32_t(quad * 32) << 16;
-    const uint32_t a_t0 = tmem_base + wg * (a_cols + d_cols);  // this warpgroup's A (lane 0)
-    const uint32_t d_t0 = a_t0 + a_cols;                       // and D
-    const uint32_t w64 = w32 / 2;
-    int32_t* Tme = T_w + warp * kQPass;
-    unsigned long long scored = 0, cands = 0;
-    uint32_t n_list = 0, mma_phase = 0;
-    float pm[PROBE ? kQPass : 1];
+    } else {
+        // ===================== workers: warpgroup wg handles sub-tiles u = wg (mod nwg) =====================
+        // Per warpgroup, software-pipelined within a strip:
+        //   expand(k+1) -> A[(k+1)&1]  while the tensor core runs MMA(k) from A[k&1]
+        //   wait MMA(k); test D; arrive a_full (A(k+1) ready, D free) -> the MMA warp issues MMA(k+1)
+        const uint32_t wg = uint32_t(warp >> 2);
+        const int quad = warp & 3;
+        const uint32_t l = uint32_t(quad * 32 + lane);  // TMEM lane == doc within the sub-tile
+        const uint32_t wt = uint32_t(threadIdx.x);      // worker thread id
+        const uint32_t lane_base = uint32_t(quad * 32) << 16;
+        const uint32_t a_t0 = tmem_base + wg * (2 * a_cols + d_cols);  // this warpgroup's A[0], A[1]
+        const uint32_t d_t = a_t0 + 2 * a_cols + lane_base;            // and D (this warp's lanes)
+        const uint32_t w64 = w32 / 2;
+        const uint32_t n_worker_warps = 4 * nwg;
+        const uint32_t pstride = p.ptop;
+        uint32_t scored = 0, cands = 0;
+        uint32_t kc = 0;  // sub-tiles processed by this warpgroup (A buffer / barrier parities)
+        float pm[PROBE ? kQPass : 1];
 #pragma unroll
-    for (int e = 0; e < (PROBE ? kQPass : 1); ++e) pm[e] = -INFINITY;
-
-    // exact FP64 rescoring of this thread's deferred candidates.  State entries
-    // (query q, doc lane l) hold key = (i << 32 | acc) of the best item so far;
-    // "higher score, then lower slot" is order-independent, so warpgroups may
-    // update the same entry in any order (64-bit CAS).
-    auto flush = [&](const StripInfo& si, const PartDesc& part) {
-        const uint64_t y_base = si.x * uint64_t(p.tpb) * p.ipt + 128 * si.h + l;
-        for (uint32_t k = 0; k < n_list; ++k) {
-            const uint32_t qi = ls_qi[k * kWorkers + wt];
-            const uint32_t q = qi >> 26, ii = qi & 0x3ffffffu;
-            const int32_t a = ls_acc[k * kWorkers + wt];
-            const double sc = __ddiv_rn(ldexp(double(a), -L), double(ls_mag[k * kWorkers + wt]));
-            if (!(sc >= theta_s[q])) continue;
-            const unsigned long long mine = (uint64_t(ii) << 32) | uint32_t(a);
-            unsigned long long* ent = st_key + q * 128 + l;
-            unsigned long long cur = *ent;
-            while (true) {
-                if (cur != kEmptyKey) {
-                    const uint32_t ci = uint32_t(cur >> 32);
-                    const double cm = double(__ldg(part.mags + y_base + uint64_t(ci) * p.tpb));
-                    const double cs = __ddiv_rn(ldexp(double(int32_t(uint32_t(cur))), -L), cm);
-                    if (!(sc > cs || (sc == cs && ii < ci))) break;  // current entry ranks first
-                }
-                const unsigned long long prev = atomicCAS(ent, cur, mine);
-                if (prev == cur) break;
-                cur = prev;
-            }
+        for (int e = 0; e < (PROBE ? kQPass : 1); ++e) pm[e] = -INFINITY;
+        {
+            // constant columns 2..7 of the X block of both A buffers (K bytes 8..31 = 255)
+            uint32_t v[8] = {0u, 0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u};
+            tmem_st8(a_t0 + lane_base + 8 * w32, v);
+            tmem_st8(a_t0 + a_cols + lane_base + 8 * w32, v);
+            tmem_wait_st();
         }
-        n_list = 0;
-    };
 
-    uint32_t u0 = 0;  // sub-tiles of earlier strips (this CTA)
-    for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
-        const StripInfo si = strip_info(p, s);
-        const PartDesc& part = p.parts[si.part];
-        // this warpgroup's sub-tiles u = u0 + i with u % kWG == wg
-        const uint32_t first = (wg + kWG - u0 % kWG) % kWG;
-        for (uint32_t i = first; i < si.n_tiles; i += kWG) {
-            const uint32_t u = u0 + i;
-            const uint32_t st_idx = u % kStages, st_phase = (u / kStages) & 1;
-            mbar_wait(full + st_idx, st_phase);
-            const uint8_t* stage = ring + st_idx * stage_bytes;
-            // ---- expand this doc into A (u8 V bytes, K-major in TMEM)
-            {
+        // expand doc `col` of ring stage `st` into A buffer `ab`; returns its magnitude and bin
+        auto expand = [&](uint32_t st, uint32_t col, uint32_t ab, float& mag, uint32_t& j) {
+            const uint8_t* stage = ring + st * stage_bytes;
+            const uint32_t a_t = a_t0 + ab * a_cols + lane_base;
+            if ((w32 & 3) == 0) {
+                // 16-byte loads: a warp reads 32 consecutive docs x 16 B = 512 B, conflict-free
+                const uint4* src = reinterpret_cast<const uint4*>(stage);
+                const uint32_t w128 = w32 / 4;
+                for (uint32_t g4 = 0; g4 < w128; ++g4) {
+                    uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
+#pragma unroll
+                    for (int t = 0; t < KP; ++t) {
+                        const uint4 v = src[(t * sw + col) * w128 + g4];
+                        w0[t] = v.x;
+                        w1[t] = v.y;
+                        w2[t] = v.z;
+                        w3[t] = v.w;
+                    }
+                    uint32_t out[16];
+                    Expand<KP, RW>::run(w0, out);
+                    Expand<KP, RW>::run(w1, out + 8);
+                    tmem_st16(a_t + 32 * g4, out);
+                    Expand<KP, RW>::run(w2, out);
+                    Expand<KP, RW>::run(w3, out + 8);
+                    tmem_st16(a_t + 32 * g4 + 16, out);
+                }
+            } else {
                 const uint2* src = reinterpret_cast<const uint2*>(stage);
-                const uint32_t a_t = a_t0 + lane_base;
                 for (uint32_t g2 = 0; g2 < w64; ++g2) {
                     uint32_t w0[KP], w1[KP];
 #pragma unroll
                     for (int t = 0; t < KP; ++t) {
-                        const uint2 v = src[(t * 128 + l) * w64 + g2];
+                        const uint2 v = src[(t * sw + col) * w64 + g2];
                         w0[t] = v.x;
                         w1[t] = v.y;
                     }
@@ -463,229 +641,311 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     tmem_st16(a_t + 16 * g2, out);
                 }
             }
-            const uint64_t slot0 = si.x * uint64_t(p.tpb) * p.ipt + uint64_t(i) * p.tpb + 128 * si.h;
-            const bool valid = slot0 + l < part.count;
-            const float mag = valid ? reinterpret_cast<const float*>(stage + KP * plane_bytes)[l] : 0.0f;
-            mbar_arrive(empty + st_idx);  // the ring slot may be refilled
-            scored += valid ? 1 : 0;
-            if (!PROBE) {
-                // this warp's integer thresholds on D (its 32 docs): acc = D + C >= t * mag
-                // is necessary for score >= theta (t = theta * 2^L); branch-free
-                const uint32_t mb = __float_as_uint(mag);
-                const float mn = __uint_as_float(__reduce_min_sync(0xffffffffu, valid ? mb : 0x7f800000u));
-                const float mx = __uint_as_float(__reduce_max_sync(0xffffffffu, mb));
-#pragma unroll
-                for (int hq = 0; hq < 2; ++hq) {
-                    const uint32_t tq = uint32_t(lane + 32 * hq);
-                    const float ta = ta_s[tq], tc = tc_s[tq];
-                    const float v = __fmaf_rd(ta, ta >= 0.0f ? mn : mx, tc);
-                    Tme[tq] = __float2int_rd(fminf(fmaxf(v, -2.1e9f), 2.1e9f));
-                }
-                __syncwarp();
-            }
-            // ---- the warpgroup's A is complete: one thread issues the MMAs
+            mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
+            j = mag_bin(mag, p.m0f, p.inv_df);
+            tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
+            mbar_arrive(empty + st);  // this sub-tile's share of the ring slot is consumed
+        };
+        // this warp's part of A is complete and its D reads are done: one arrival per warp
+        auto arrive_a = [&]() {
             tmem_wait_st();
             tc_fence_before();
-            named_bar(1 + int(wg), 128);
-            if ((threadIdx.x & 127) == 0) {
-                tc_fence_after();
-                const uint32_t idesc = idesc_i8(128, p.n_pad);
-                const uint32_t b_base = smem_u32(bsm);
-                for (uint32_t kb = 0; kb < n_kb; ++kb)
-                    mma_i8(d_t0, a_t0 + 8 * kb, smem_desc(b_base + kb * p.n_pad * 32), idesc, kb > 0);
-                mma_commit(mma_done + wg);
-            }
-            mbar_wait(mma_done + wg, mma_phase);
-            mma_phase ^= 1;
-            tc_fence_after();
-            const uint32_t d_t = d_t0 + lane_base;
-            const float scale = PROBE ? __fdiv_rn(ldexpf(1.0f, -L), mag) : 0.0f;
-#pragma unroll
-            for (int c = 0; c < kQPass / 32; ++c) {
-                int32_t acc[32];
-                tmem_ld32(d_t + 32 * c, acc);
-                tmem_wait_ld();
-                if (PROBE) {
-                    if (valid) {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            pm[32 * c + e] = fmaxf(pm[32 * c + e], float(acc[e] + cq_s[32 * c + e]) * scale);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full + wg);
+        };
+
+        uint32_t u0 = 0;       // sub-tiles of earlier strips (this CTA)
+        uint32_t tiles0 = 0;   // ring stages (tiles) of earlier strips (this CTA)
+        for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
+            const StripInfo si = strip_info(p, s);
+            const PartDesc& part = p.parts[si.part];
+            const uint32_t n_sub = si.n_tiles * spt;
+            const uint64_t lim = part.count > si.base ? part.count - si.base : 0;  // valid: i*tpb + col < lim
+            // this warpgroup's sub-tiles k = first, first + nwg, ... (u = u0 + k, u % nwg == wg)
+            uint32_t k = (wg + nwg - u0 % nwg) % nwg;
+            if (k < n_sub) {
+                // ring position of the tile holding sub-tile k, advanced incrementally
+                uint32_t ti = k / spt;
+                uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
+                auto seek = [&](uint32_t t_new) {
+                    for (; ti < t_new; ++ti)
+                        if (++st_idx == nst) {
+                            st_idx = 0;
+                            st_ph ^= 1;
+                        }
+                };
+                RBE_CLK_DECL(c1);
+                float mag, mag_n = 0.0f;
+                uint32_t j, j_n = 0;
+                uint32_t col = (k % spt) * 128 + l, col_n = 0;
+                mbar_wait(full + st_idx, st_ph);
+                expand(st_idx, col, kc & 1, mag, j);
+                arrive_a();
+                while (true) {
+                    const uint32_t k_n = k + nwg;
+                    const bool has_next = k_n < n_sub;
+                    const uint32_t i = k / spt;
+                    RBE_CLK(c0);
+                    if (has_next) {
+                        seek(k_n / spt);
+                        col_n = (k_n % spt) * 128 + l;
+                        mbar_wait(full + st_idx, st_ph);
+                        RBE_CLK_SET(c1);
+                        expand(st_idx, col_n, (kc + 1) & 1, mag_n, j_n);
+                    } else {
+                        RBE_CLK_COPY(c1, c0);
                     }
-                    continue;
-                }
-                // stage 1: one ISETP per pair against this warp's thresholds,
-                // accumulated into one predicate per 16-query group
-                bool h0 = false, h1 = false;
+                    RBE_CLK(c2);
+                    const bool valid = uint64_t(i) * p.tpb + col < lim;
+                    scored += valid ? 1 : 0;
+                    mbar_wait_sleep(mma_done + wg, kc & 1);
+                    tc_fence_after();
+                    RBE_CLK(c3);
+                    if (PROBE) {
+                        // F = lambda acc; per-thread maxima of the (float) score
+                        const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    h0 |= acc[e] >= Tme[32 * c + e];
-                    h1 |= acc[16 + e] >= Tme[32 * c + 16 + e];
-                }
-                uint32_t gm = valid ? (uint32_t(h0) | (uint32_t(h1) << 1)) : 0u;
-                const uint32_t any = __reduce_or_sync(0xffffffffu, gm);
-                if (!any) continue;
+                        for (int c = 0; c < kQPass / 16; ++c) {
+                            int32_t F[16];
+                            tmem_ld16(d_t + 16 * c, F);
+                            tmem_wait_ld();
+                            if (valid) {
 #pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    if (!(any & (1u << g))) continue;
-                    uint32_t mask = 0;
-                    if (gm & (1u << g)) {
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) mask |= uint32_t(acc[16 * g + e] >= Tme[32 * c + 16 * g + e]) << e;
-                    }
-                    while (mask) {
-                        const int e = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        int32_t a = 0;
-#pragma unroll
-                        for (int k2 = 0; k2 < 16; ++k2)
-                            if (k2 == e) a = acc[16 * g + k2];
-                        const uint32_t q = uint32_t(32 * c + 16 * g + e);
-                        const int32_t accq = a + cq_s[q];
-                        // stage 2: per-doc float test (conservative), before any FP64 work
-                        const float t = t2l_s[q];
-                        const float need = t >= 0.0f ? __fmul_rd(__fmul_rd(t, mag), 0.99999f)
-                                                     : __fmul_rd(__fmul_rd(t, mag), 1.00001f);
-                        if (t > -INFINITY && float(accq) < need - 2.0f) continue;
-                        ++cands;
-                        if (n_list == kList) flush(si, part);
-                        ls_qi[n_list * kWorkers + wt] = (q << 26) | i;
-                        ls_acc[n_list * kWorkers + wt] = accq;
-                        ls_mag[n_list * kWorkers + wt] = mag;
-                        ++n_list;
-                    }
-                }
-            }
-            tc_fence_before();  // our D reads are complete before the next MMA into D
-        }
-        u0 += si.n_tiles;
-        // ================= strip end (all worker warps) =================
-        if (PROBE) {
-            // merge the warpgroups' per-lane maxima, then per query keep the top
-            // kProbeTop per-thread maxima of the strip (distinct threads)
-            for (uint32_t w = 0; w < uint32_t(kWG); ++w) {
-                if (w == wg) {
-#pragma unroll
-                    for (int e = 0; e < kQPass; ++e) {
-                        float* m = pmax + e * 128 + l;
-                        *m = fmaxf(*m, pm[e]);
-                        pm[e] = -INFINITY;
-                    }
-                }
-                named_bar(kAllBar, kWorkers);
-            }
-            for (uint32_t q = uint32_t(warp); q < p.nq; q += kWorkerWarps) {
-                float v[4];
-#pragma unroll
-                for (int k2 = 0; k2 < 4; ++k2) v[k2] = pmax[q * 128 + 32 * k2 + lane];
-                for (int r = 0; r < kProbeTop; ++r) {
-                    const float best = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-                    float m = best;
-                    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-                    const unsigned holder = __ballot_sync(0xffffffffu, best == m);
-                    if (lane == __ffs(holder) - 1) {
-                        bool done = false;
-#pragma unroll
-                        for (int k2 = 0; k2 < 4; ++k2)
-                            if (!done && v[k2] == m) {
-                                v[k2] = -INFINITY;
-                                done = true;
+                                for (int e = 0; e < 16; ++e)
+                                    pm[16 * c + e] = fmaxf(pm[16 * c + e], float(F[e]) * scale);
                             }
+                        }
+                    } else {
+                        // F >= 0 is necessary for score >= theta: AND the sign bits, 32 queries
+                        // at a time; the rare passing groups are re-read from TMEM
+                        uint32_t gmask = 0;  // bit g: some F >= 0 among queries [8g, 8g+8)
+#pragma unroll
+                        for (int h = 0; h < kQPass / 32; ++h) {
+                            int32_t F[32];
+                            tmem_ld32(d_t + 32 * h, F);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                uint32_t a = uint32_t(F[8 * g]);
+#pragma unroll
+                                for (int e = 1; e < 8; ++e) a &= uint32_t(F[8 * g + e]);
+                                gmask |= (~a >> 31) << (4 * h + g);
+                            }
+                        }
+                        // groups with a passing pair in any valid lane of the warp (tcgen05.ld is
+                        // warp-collective, so the whole warp re-reads them together)
+                        uint32_t wmask = __reduce_or_sync(0xffffffffu, valid ? gmask : 0u);
+                        while (wmask) {
+                            const int g = __ffs(wmask) - 1;
+                            wmask &= wmask - 1;
+                            int32_t v[8];
+                            tmem_ld8(d_t + 8 * g, v);
+                            tmem_wait_ld();
+                            if (!valid || !((gmask >> g) & 1)) continue;
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                if (v[e] < 0) continue;
+                                ++cands;
+                                const uint32_t q = uint32_t(8 * g + e);
+                                const int32_t X = xc_s[q] - xe_s[q] * int32_t(j) - xg_s[q] * int32_t(j >> 4);
+                                const int32_t num = v[e] - X;
+                                if (num & ((1 << p.lam_shift) - 1)) atomicAdd(p.error, 1u);
+                                const int32_t a = (num >> p.lam_shift) + cq_s[q];
+                                // defer to the strip end (exact FP64 scoring in bulk); score now if full
+                                const uint32_t pos = atomicAdd(cq_count, 1u);
+                                if (pos < kCandQueue)
+                                    cqueue[pos] = make_uint2((q << 26) | i, (col << 24) | (uint32_t(a) & 0xffffffu));
+                                else
+                                    take_candidate(a, q, mag, i, col, sw, theta_s, st_key,
+                                                   part.mags + si.base + col, p.tpb, L);
+                            }
+                        }
                     }
-                    if (lane == 0) p.probe_out[uint64_t(p.q0 + q) * p.n_strips * kProbeTop + s * kProbeTop + r] = m;
+                    RBE_CLK(c4);
+                    ++kc;
+                    if (!has_next) break;
+                    arrive_a();
+#ifdef RBE_PHASE_PROF
+                    if (p.prof && lane == 0 && quad == 1) {
+                        long long c5 = clock64();
+                        unsigned long long* pr = p.prof + (uint64_t(blockIdx.x) * kMaxWG + wg) * 8;
+                        pr[0] += c1 - c0;  // wait full
+                        pr[1] += c2 - c1;  // expand
+                        pr[2] += c3 - c2;  // wait mma
+                        pr[3] += c4 - c3;  // epilogue
+                        pr[4] += c5 - c4;  // arrive
+                        pr[5] += 1;
+                    }
+#endif
+                    k = k_n;
+                    col = col_n;
+                    mag = mag_n;
+                    j = j_n;
+                }
+                tc_fence_before();
+            }
+            u0 += n_sub;
+            tiles0 += si.n_tiles;
+            // ================= strip end (all worker warps) =================
+            if (PROBE) {
+                // merge the warpgroups' per-lane maxima: in the probe each warpgroup's lanes
+                // always hold the same logical threads (host: nwg == spt when spt > 1)
+                {
+                    const uint32_t colp = (wg % spt) * 128 + l;
+                    for (uint32_t w = 0; w < nwg; ++w) {
+                        if (w == wg) {
+#pragma unroll
+                            for (int e = 0; e < kQPass; ++e) {
+                                float* m = pmax + e * sw + colp;
+                                *m = fmaxf(*m, pm[e]);
+                                pm[e] = -INFINITY;
+                            }
+                        }
+                        named_bar(kAllBar, n_workers);
+                    }
+                }
+                // per query keep the top ptop per-thread maxima of the strip (distinct threads)
+                const uint32_t vpl = sw / 32;  // values per lane
+                for (uint32_t q = uint32_t(warp); q < p.nq; q += n_worker_warps) {
+                    float v[8];
+#pragma unroll
+                    for (int k2 = 0; k2 < 8; ++k2) v[k2] = uint32_t(k2) < vpl ? pmax[q * sw + 32 * k2 + lane] : -INFINITY;
+                    for (uint32_t r = 0; r < pstride; ++r) {
+                        float best = v[0];
+#pragma unroll
+                        for (int k2 = 1; k2 < 8; ++k2) best = fmaxf(best, v[k2]);
+                        float m = best;
+                        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+                        const unsigned holder = __ballot_sync(0xffffffffu, best == m);
+                        if (lane == __ffs(holder) - 1) {
+                            bool done = false;
+#pragma unroll
+                            for (int k2 = 0; k2 < 8; ++k2)
+                                if (!done && v[k2] == m) {
+                                    v[k2] = -INFINITY;
+                                    done = true;
+                                }
+                        }
+                        if (lane == 0) p.probe_out[(uint64_t(p.q0 + q) * p.n_strips + s) * pstride + r] = m;
+                    }
+                }
+                named_bar(kAllBar, n_workers);
+                for (uint32_t e = wt; e < kQPass * sw; e += n_workers) pmax[e] = -INFINITY;
+                named_bar(kAllBar, n_workers);
+                continue;
+            }
+            named_bar(kAllBar, n_workers);
+            // exact FP64 scoring of the strip's deferred candidates (all worker threads)
+            {
+                const uint32_t nc = min(*cq_count, uint32_t(kCandQueue));
+                for (uint32_t e = wt; e < nc; e += n_workers) {
+                    const uint2 c = cqueue[e];
+                    const uint32_t q = c.x >> 26, ii = c.x & 0x3ffffffu, cc = c.y >> 24;
+                    const int32_t a = int32_t(c.y << 8) >> 8;
+                    const float m = __ldg(part.mags + si.base + cc + uint64_t(ii) * p.tpb);
+                    take_candidate(a, q, m, ii, cc, sw, theta_s, st_key, part.mags + si.base + cc, p.tpb, L);
                 }
             }
-            named_bar(kAllBar, kWorkers);
-            for (uint32_t e = wt; e < kQPass * 128; e += kWorkers) pmax[e] = -INFINITY;
-            named_bar(kAllBar, kWorkers);
-            continue;
-        }
-        flush(si, part);
-        named_bar(kAllBar, kWorkers);
-        // emit the strip's survivors >= theta (one per (query, logical thread))
-        for (uint32_t e = wt; e < p.nq * 128; e += kWorkers) {
-            const unsigned long long key = st_key[e];
-            if (key == kEmptyKey) continue;
-            st_key[e] = kEmptyKey;
-            const uint32_t q = e / 128, el = e % 128;
-            const uint32_t ii = uint32_t(key >> 32);
-            const int32_t a = int32_t(uint32_t(key));
-            const uint64_t slot = si.x * uint64_t(p.tpb) * p.ipt + 128 * si.h + el + uint64_t(ii) * p.tpb;
-            const double sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
-            if (!(sc >= theta_s[q])) continue;  // theta may have risen since it was queued
-            const unsigned long long pos = atomicAdd(p.surv_count + p.q0 + q, 1ull);
-            if (pos < p.surv_cap) {
-                Result r;
-                r.score = sc;
-                r.id = part.ids[slot];
-                r.acc = a;
-                r.partition = part.ordinal;
-                r.valid = 1;
-                p.surv[uint64_t(p.q0 + q) * p.surv_cap + pos] = r;
+            named_bar(kAllBar, n_workers);
+            if (wt == 0) *cq_count = 0;
+            // emit the strip's survivors >= theta (one per (query, logical thread))
+            for (uint32_t e = wt; e < p.nq * sw; e += n_workers) {
+                const unsigned long long key = st_key[e];
+                if (key == kEmptyKey) continue;
+                st_key[e] = kEmptyKey;
+                const uint32_t q = e / sw, cc = e % sw;
+                const uint32_t ii = uint32_t(key >> 32);
+                const int32_t a = int32_t(uint32_t(key));
+                const uint64_t slot = si.base + cc + uint64_t(ii) * p.tpb;
+                const double sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
+                if (!(sc >= theta_s[q])) continue;  // theta may have risen since it was queued
+                const unsigned long long pos = atomicAdd(p.surv_count + p.q0 + q, 1ull);
+                if (pos < p.surv_cap) {
+                    Result r;
+                    r.score = sc;
+                    r.id = part.ids[slot];
+                    r.acc = a;
+                    r.partition = part.ordinal;
+                    r.valid = 1;
+                    p.surv[uint64_t(p.q0 + q) * p.surv_cap + pos] = r;
+                }
+                // every emitted survivor is a final survivor of a distinct logical thread
+                const double dq = p.delta_h[p.q0 + q];
+                double fb = floor((sc - p.theta0[p.q0 + q]) / dq);
+                fb = fb < 0.0 ? 0.0 : (fb > double(kBins - 1) ? double(kBins - 1) : fb);
+                atomicAdd(p.hist + uint64_t(p.q0 + q) * kBins + int(fb), 1u);
             }
-            // every emitted survivor is a final survivor of a distinct logical thread
-            const double dq = p.delta[p.q0 + q];
-            double fb = floor((sc - p.theta0[p.q0 + q]) / dq);
-            fb = fb < 0.0 ? 0.0 : (fb > double(kBins - 1) ? double(kBins - 1) : fb);
-            atomicAdd(p.hist + uint64_t(p.q0 + q) * kBins + int(fb), 1u);
-        }
-        named_bar(kAllBar, kWorkers);
-        // ---- dynamic theta: raise theta_q to the lower edge of the highest bin
-        // whose suffix count of emitted survivors reaches n (a valid lower bound
-        // on the final n-th survivor score).  Worker warp w refreshes q = w (mod 12).
-        for (uint32_t q = uint32_t(warp); q < p.nq; q += kWorkerWarps) {
-            const uint32_t* hp = p.hist + uint64_t(p.q0 + q) * kBins;
-            uint32_t sh = __ldcg(hp + 32 + lane), sl2 = __ldcg(hp + lane);
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t a = __shfl_down_sync(0xffffffffu, sh, off);
-                const uint32_t c = __shfl_down_sync(0xffffffffu, sl2, off);
-                if (lane + off < 32) {
-                    sh += a;
-                    sl2 += c;
+            named_bar(kAllBar, n_workers);
+            // ---- dynamic theta: raise theta_q to the lower edge of the highest bin
+            // whose suffix count of emitted survivors reaches n (a valid lower bound
+            // on the final n-th survivor score), and rewrite the query's X block.
+            bool wrote = false;
+            for (uint32_t q = uint32_t(warp); q < p.nq; q += n_worker_warps) {
+                const uint32_t* hp = p.hist + uint64_t(p.q0 + q) * kBins;
+                uint32_t sh = __ldcg(hp + 32 + lane), sl2 = __ldcg(hp + lane);
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t a = __shfl_down_sync(0xffffffffu, sh, off);
+                    const uint32_t c = __shfl_down_sync(0xffffffffu, sl2, off);
+                    if (lane + off < 32) {
+                        sh += a;
+                        sl2 += c;
+                    }
+                }
+                const uint32_t tot_hi = __shfl_sync(0xffffffffu, sh, 0);
+                sl2 += tot_hi;
+                const unsigned mh = __ballot_sync(0xffffffffu, uint64_t(sh) >= p.n);
+                const unsigned ml = __ballot_sync(0xffffffffu, uint64_t(sl2) >= p.n);
+                int B = -1;
+                if (mh) B = 32 + (31 - __clz(mh));
+                else if (ml) B = 31 - __clz(ml);
+                if (lane == 0 && B > 0) {
+                    const double edge = p.theta0[p.q0 + q] + double(B) * p.delta_h[p.q0 + q];
+                    const double th = edge - fabs(edge) * 1e-9 - 0x1p-60;
+                    if (th > theta_s[q]) {
+                        theta_s[q] = th;
+                        const XCoef x = x_coeffs(th, cq_s[q], L, lam, p.m0, p.delta, p.mmax);
+                        xc_s[q] = x.c;
+                        xe_s[q] = x.e;
+                        xg_s[q] = x.g;
+                        write_xrow(bsm, p.n_pad, w32, q, x);
+                        wrote = true;
+                    }
                 }
             }
-            const uint32_t tot_hi = __shfl_sync(0xffffffffu, sh, 0);
-            sl2 += tot_hi;
-            const unsigned mh = __ballot_sync(0xffffffffu, uint64_t(sh) >= p.n);
-            const unsigned ml = __ballot_sync(0xffffffffu, uint64_t(sl2) >= p.n);
-            int B = -1;
-            if (mh) B = 32 + (31 - __clz(mh));
-            else if (ml) B = 31 - __clz(ml);
-            if (lane == 0 && B > 0) {
-                const double edge = p.theta0[p.q0 + q] + double(B) * p.delta[p.q0 + q];
-                const double th = edge - fabs(edge) * 1e-9 - 0x1p-60;
-                if (th > theta_s[q]) {
-                    theta_s[q] = th;
-                    const float t = __double2float_rd(ldexp(th, L));
-                    t2l_s[q] = t;
-                    set_filter_coeffs(t, cq_s[q], ta_s + q, tc_s + q);
-                }
+            if (wrote) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            named_bar(kAllBar, n_workers);
+        }
+        if (!PROBE) {
+            unsigned long long sc64 = (unsigned long long)scored * p.nq, cd64 = cands;
+            for (int off = 16; off > 0; off >>= 1) {
+                sc64 += __shfl_xor_sync(0xffffffffu, sc64, off);
+                cd64 += __shfl_xor_sync(0xffffffffu, cd64, off);
             }
-        }
-    }
-    if (!PROBE) {
-        scored *= p.nq;
-        for (int off = 16; off > 0; off >>= 1) {
-            scored += __shfl_xor_sync(0xffffffffu, scored, off);
-            cands += __shfl_xor_sync(0xffffffffu, cands, off);
-        }
-        if (lane == 0) {
-            atomicAdd(p.scored, scored);
-            atomicAdd(p.candidates, cands);
+            if (lane == 0) {
+                atomicAdd(p.scored, sc64);
+                atomicAdd(p.candidates, cd64);
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (warp == producer_warp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    }
 }
 
 // ------------------------------------------------------------ query operand
-// natural query words [Q][qp][wpp] -> B image bytes (2*rq_j as s8) in the
-// K-major SWIZZLE_NONE core-matrix layout, per 64-query pass:
+// natural query words [Q][qp][wpp] -> B image bytes (2 lambda rq_j as s8) of
+// the data K blocks in the K-major SWIZZLE_NONE core-matrix layout, per
+// 64-query pass:
 //   pass P, K block kb, row r (query), k byte: offset = P*passbytes + kb*(n_pad*32)
 //     + (r/8)*256 + ((k%32)/16)*128 + (r%8)*16 + k%16
 // and C_q (int32).  One CTA per query.
 __global__ void prepare_queries_tensor_kernel(const uint64_t* __restrict__ q, uint32_t Q, uint32_t qp, uint32_t kp,
                                               uint32_t dim, uint32_t wpp, uint32_t rw, uint32_t n_pad,
-                                              uint8_t* __restrict__ bimg, int32_t* __restrict__ cq) {
+                                              uint32_t lam_shift, uint8_t* __restrict__ bimg,
+                                              int32_t* __restrict__ cq) {
     const uint32_t qi = blockIdx.x;
     const uint32_t K = 64 * wpp;
     const uint32_t pass = qi / kQPass, r = qi % kQPass;
@@ -702,7 +962,7 @@ __global__ void prepare_queries_tensor_kernel(const uint64_t* __restrict__ q, ui
         const uint32_t kb = k / 32, kk = k % 32;
         const size_t off = pass * pass_bytes + size_t(kb) * n_pad * 32 + (r / 8) * 256 + (kk / 16) * 128 + (r % 8) * 16 +
                            kk % 16;
-        bimg[off] = uint8_t(int8_t(2 * rq));
+        bimg[off] = uint8_t(int8_t(rq * (2 << lam_shift)));
     }
     part[threadIdx.x] = sum;
     __syncthreads();
@@ -804,18 +1064,22 @@ __global__ void __launch_bounds__(1024) theta_kernel(const float* __restrict__ p
     }
 }
 
-uint64_t count_strips(const Shape&, const rbe_scan_geometry& g, uint64_t count) {
+// strip width: 256 logical threads (one 256-doc contiguous stage per tile, the
+// bulk-copy size that reaches full HBM bandwidth) when the block width allows it
+uint32_t strip_width(const rbe_scan_geometry& g) { return g.threads_per_block % 256 == 0 ? 256u : 128u; }
+
+uint64_t count_strips(const rbe_scan_geometry& g, uint64_t count) {
     const uint64_t per_block = uint64_t(g.threads_per_block) * g.items_per_thread;
     uint64_t blocks = per_block ? (count + per_block - 1) / per_block : 0;
     if (blocks > g.blocks) blocks = g.blocks;
-    return blocks * (g.threads_per_block / 128);
+    return blocks * (g.threads_per_block / strip_width(g));
 }
 
 template <int KP, bool RW, bool PROBE>
 void launch_kernel(const TensorParams& tp, size_t smem, int grid, cudaStream_t st) {
     auto k = tensor_scan_kernel<KP, RW, PROBE>;
     RBE_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k<<<grid, kThreads, smem, st>>>(tp);
+    k<<<grid, 32 * (5 * tp.nwg + 1), smem, st>>>(tp);
     RBE_CK(cudaGetLastError());
 }
 
@@ -840,8 +1104,42 @@ void dispatch(uint32_t kp, bool rw, const TensorParams& tp, size_t smem, int gri
 #undef RBE_CASE
 }
 
-size_t kernel_smem(uint32_t kp, uint32_t w32, uint32_t n_pad, bool probe) {
-    return smem_layout(kp, w32, n_pad, probe).total;
+constexpr size_t kSmemLimit = 227 * 1024;
+
+// worker warpgroups: as many as the TMEM budget (512 columns) allows
+uint32_t pick_nwg(uint32_t w32) {
+    for (uint32_t nwg = kMaxWG; nwg >= 2; --nwg)
+        if (nwg * (2 * 8 * (w32 + 1) + kQPass) <= 512) return nwg;
+    return 0;
+}
+
+// ring depth: as many stages (<= kStages) as shared memory allows
+uint32_t pick_stages(uint32_t kp, uint32_t w32, uint32_t sw) {
+    for (uint32_t ns = kStages; ns >= 2; --ns)
+        if (smem_layout(kp, w32, kQPass, ns, sw, false).total <= kSmemLimit) return ns;
+    return 0;
+}
+
+// lambda = 2^shift: the largest with |2 lambda rq| <= 127 and the data part of
+// F strictly inside the range the X block can offset (all-pass / none-pass).
+int pick_lam_shift(const Shape& s, uint32_t qp) {
+    const uint64_t rqmax = s.rw ? ((1ull << qp) - 1) : qp;
+    const uint64_t vmax = s.rw ? ((1ull << s.kp) - 1) : s.kp;
+    const uint64_t K = 32ull * s.w32;
+    for (int sh = 6; sh >= 0; --sh) {
+        const uint64_t sigma = 2ull << sh;
+        if (sigma * rqmax <= 127 && sigma * rqmax * vmax * K < uint64_t(kXMax)) return sh;
+    }
+    return -1;
+}
+
+rbe_scan_geometry g_of(const ScanArgs& a) {
+    rbe_scan_geometry g{};
+    g.blocks = a.blocks;
+    g.threads_per_block = a.tpb;
+    g.items_per_thread = a.ipt;
+    g.queue_length = a.ql;
+    return g;
 }
 
 int sm_count() {
@@ -864,7 +1162,9 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
     if (s.rw ? qp > 6 : qp > 63) return no("query planes exceed the s8 operand range");
     if (s.wpp > 4) return no("dim > 256");
     if (Q == 0) return no("no queries");
-    if (kernel_smem(s.kp, s.w32, kQPass, false) > 227 * 1024) return no("shared memory");
+    if (pick_nwg(s.w32) == 0) return no("tensor memory");
+    if (pick_stages(s.kp, s.w32, strip_width(g)) == 0) return no("shared memory");
+    if (pick_lam_shift(s, qp) < 0) return no("accumulator range exceeds the threshold block");
     if (g.items_per_thread >= (1u << 26)) return no("items_per_thread >= 2^26");
     return true;
 }
@@ -879,14 +1179,17 @@ TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geom
     pl.prefix.assign(counts.size() + 1, 0);
     const uint64_t threads = uint64_t(g.blocks) * g.threads_per_block;
     for (size_t i = 0; i < counts.size(); ++i) {
-        pl.prefix[i + 1] = pl.prefix[i] + count_strips(s, g, counts[i]);
+        pl.prefix[i + 1] = pl.prefix[i] + count_strips(g, counts[i]);
         pl.surv_cap += std::min<uint64_t>(counts[i], threads);
     }
     pl.surv_cap = std::max<uint64_t>(pl.surv_cap, 1);
     pl.n_strips = pl.prefix.back();
     const uint32_t passes = (Q + kQPass - 1) / kQPass;
     pl.query_bytes = size_t(passes) * kQPass * 64 * s.wpp + size_t(Q) * 4 + 256;
-    pl.probe_bytes = size_t(Q) * pl.n_strips * kProbeTop * sizeof(float) + 256;
+    // probe values per (query, strip): enough that n of them exist when the probe covers
+    // the corpus thinly (a few strips), at least 4
+    pl.ptop = uint32_t(std::min<uint64_t>(32, std::max<uint64_t>(4, pl.n_strips ? (2 * n + pl.n_strips - 1) / pl.n_strips : 4)));
+    pl.probe_bytes = size_t(Q) * pl.n_strips * pl.ptop * sizeof(float) + 256;
     pl.threshold_bytes = size_t(Q) * (32 + kBins * 4) + 64;
     pl.state_bytes = sizeof(uint64_t) * pl.prefix.size() + 64;
     return pl;
@@ -902,21 +1205,29 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
                            st));
     const uint32_t passes = (Q + kQPass - 1) / kQPass;
     const uint32_t n_pad = kQPass;
+    const int lam_shift = pick_lam_shift(s, a.qp);
+    if (lam_shift < 0) throw std::invalid_argument("tensor scan: accumulator range exceeds the threshold block");
     uint8_t* bimg = static_cast<uint8_t*>(d_qtensor);
     const size_t pass_bytes = size_t(n_pad) * 64 * s.wpp;
     int32_t* cq = reinterpret_cast<int32_t*>(bimg + size_t(passes) * pass_bytes);
     double* theta = static_cast<double*>(d_thresholds);
     double* t2l = theta + Q;
     double* theta0 = t2l + Q;
-    double* delta = theta0 + Q;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(delta + Q);
+    double* delta_h = theta0 + Q;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(delta_h + Q);
     RBE_CK(cudaMemsetAsync(hist, 0, size_t(Q) * kBins * 4, st));
     RBE_CK(cudaMemsetAsync(bimg, 0, size_t(passes) * pass_bytes, st));
-    prepare_queries_tensor_kernel<<<Q, 256, 0, st>>>(d_queries, Q, a.qp, s.kp, s.dim, s.wpp, s.rw, n_pad, bimg, cq);
+    prepare_queries_tensor_kernel<<<Q, 256, 0, st>>>(d_queries, Q, a.qp, s.kp, s.dim, s.wpp, s.rw, n_pad,
+                                                     uint32_t(lam_shift), bimg, cq);
     RBE_CK(cudaGetLastError());
     uint32_t launches = 1;
-    const uint64_t per_query = n_strips * kProbeTop;
+    const uint64_t per_query = n_strips * plan.ptop;
     float* probe = static_cast<float*>(d_probe);
+
+    // magnitude bins: m0 + Delta j <= m for j = floor((m - m0)/Delta - 1e-3) in [0, 255]
+    const double m0 = double(a.mag_lo), mmax = double(a.mag_hi);
+    double delta = (mmax - m0) / 255.0;
+    if (!(delta > 0.0)) delta = std::max(m0, 1e-30) * 0x1p-20;
 
     TensorParams tp{};
     tp.parts = a.parts;
@@ -925,11 +1236,21 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.tpb = a.tpb;
     tp.ipt = a.ipt;
     tp.w32 = s.w32;
+    tp.nwg = pick_nwg(s.w32);
+    if (const char* e = getenv("RBE_NWG")) tp.nwg = std::min<uint32_t>(tp.nwg, uint32_t(atoi(e)));
+    tp.sw = strip_width(g_of(a));
+    tp.nstages = pick_stages(s.kp, s.w32, tp.sw);
+    tp.ptop = plan.ptop;
     tp.n_pad = n_pad;
     tp.L = s.rw ? (a.qp + s.kp - 2) : 0;
+    tp.lam_shift = uint32_t(lam_shift);
+    tp.m0 = m0;
+    tp.delta = delta;
+    tp.mmax = mmax;
+    tp.m0f = a.mag_lo;
+    tp.inv_df = float(1.0 / delta);
     tp.cq = cq;
     tp.theta = theta;
-    tp.t2l = t2l;
     tp.n_strips = n_strips;
     tp.probe_out = probe;
     tp.surv = a.surv;
@@ -937,27 +1258,54 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.surv_cap = a.surv_cap;
     tp.scored = a.scored;
     tp.candidates = d_candidates;
+    tp.error = a.error;
     tp.hist = hist;
-    tp.delta = delta;
+    tp.delta_h = delta_h;
     tp.theta0 = theta0;
     tp.n = plan.n;
     if (n_strips == 0) return launches;
     const int grid = int(std::min<uint64_t>(n_strips, uint64_t(sm_count())));
+    static unsigned long long* d_prof = nullptr;
+    const bool prof = getenv("RBE_PROF") != nullptr;
+    if (prof && !d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 1024 * kMaxWG * 8));
     for (uint32_t ps = 0; ps < passes; ++ps) {
         tp.q0 = ps * kQPass;
         tp.nq = std::min<uint32_t>(kQPass, Q - tp.q0);
         tp.bimg = bimg + size_t(ps) * pass_bytes;
         // probe pass -> theta
         tp.probe_tiles = plan.probe_tiles;
-        dispatch<true>(s.kp, s.rw != 0, tp, kernel_smem(s.kp, s.w32, n_pad, true), grid, st);
+        {
+            // probe: each warpgroup's lanes must always hold the same logical threads
+            TensorParams pp = tp;
+            if (tp.sw > 128) pp.nwg = tp.sw / 128;
+            dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
+        }
         const size_t tsm = size_t(kThetaCap) * 4;
         RBE_CK(cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsm)));
         theta_kernel<<<tp.nq, 1024, tsm, st>>>(probe + uint64_t(tp.q0) * per_query, per_query, plan.n, tp.L,
-                                               theta + tp.q0, t2l + tp.q0, theta0 + tp.q0, delta + tp.q0);
+                                               theta + tp.q0, t2l + tp.q0, theta0 + tp.q0, delta_h + tp.q0);
         RBE_CK(cudaGetLastError());
         // main pass
         tp.probe_tiles = 0;
-        dispatch<false>(s.kp, s.rw != 0, tp, kernel_smem(s.kp, s.w32, n_pad, false), grid, st);
+        if (prof) {
+            RBE_CK(cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * grid * kMaxWG * 8, st));
+            tp.prof = d_prof;
+        }
+        dispatch<false>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, false).total, grid, st);
+        tp.prof = nullptr;
+        if (prof) {
+            std::vector<unsigned long long> h(size_t(grid) * kMaxWG * 8);
+            RBE_CK(cudaMemcpyAsync(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost, st));
+            RBE_CK(cudaStreamSynchronize(st));
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int b = 0; b < grid; ++b)
+                for (int w = 0; w < kMaxWG; ++w)
+                    for (int k = 0; k < 8; ++k) acc[k] += double(h[(size_t(b) * kMaxWG + w) * 8 + k]);
+            fprintf(stderr, "[rbe prof] producer: waiting for free slots %.1f%% of its time\n", 100.0 * acc[6] / acc[7]);
+            fprintf(stderr, "[rbe prof] per WG sub-tile cycles: wait_full %.0f expand %.0f wait_mma %.0f epilogue %.0f "
+                            "bar+issue %.0f (n=%.0f)\n",
+                    acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[4] / acc[5], acc[5]);
+        }
         launches += 3;
     }
     return launches;

@@ -16,7 +16,8 @@ struct TensorScanPlan {
     uint32_t Q = 0, qp = 0;
     uint64_t n = 0;
     uint32_t probe_tiles = 0;
-    uint64_t n_strips = 0;            // 128-doc strips (128 logical threads of one block)
+    uint32_t ptop = 4;                // probe values kept per (query, strip)
+    uint64_t n_strips = 0;            // strips (128 or 256 logical threads of one block)
     std::vector<uint64_t> prefix;     // strips per local partition, cumulative [n_parts + 1]
     uint64_t surv_cap = 0;            // per-query survivor capacity (<= 1 per logical thread)
     size_t query_bytes = 0, probe_bytes = 0, threshold_bytes = 0, state_bytes = 0;
