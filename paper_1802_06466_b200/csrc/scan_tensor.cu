@@ -61,13 +61,16 @@
 namespace rbe_dev {
 namespace {
 
-constexpr int kStages = 12;          // ring of 128-doc sub-tiles
-constexpr int kMaxWG = 3;            // worker warpgroups (13 warps: <= 4 per SMSP -> 128 registers)
-constexpr int kMaxThreads = 32 * (5 * kMaxWG + 1);  // workers + producer + MMA issuers
-constexpr uint32_t kCandQueue = 512;  // deferred candidates per strip (shared memory; overflow is scored at once)
-constexpr int kAllBar = 8;           // named barrier of all worker threads (1..nwg: per warpgroup)
+constexpr int kStages = 12;          // max ring depth (stages of sw docs)
+constexpr int kThreads = 640;        // 20 warps (roles: see tensor_scan_kernel), 96 registers each
+constexpr int kProducerWarp = 16;
+constexpr int kMmaWarp0 = 17;
+constexpr int kMmaWarps = 2;         // MMA issuer warps 17..19 (issue latency, not the tensor pipe, bounds one issuer)
+constexpr int kSlots = 4;            // A and D slots in TMEM (sub-tiles in flight)
+constexpr uint32_t kCandQueue = 4096;  // deferred candidates per strip (shared memory; overflow is scored at once)
+constexpr int kEpiBar = 8;           // named barrier of the 256 epilogue threads
 constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
-constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr uint32_t kEmptyKey = ~0u;      // state key: (i << 23) | (acc & 0x7fffff), i < 511, |acc| < 2^22
 constexpr int kBins = 64;            // dynamic-theta histogram bins per query
 constexpr int kHiCols = 24;          // X block: K bytes 8..31 hold 255 (the c_q "high" part)
 constexpr int32_t kXMax = 255 * kHiCols * 127 + 127;  // largest |X| the block can encode
@@ -79,8 +82,12 @@ struct TensorParams {
     uint32_t n_parts;
     uint32_t tpb, ipt;
     uint32_t w32;                  // u32 words per doc plane (= data K blocks)
-    uint32_t nwg;                  // worker warpgroups
     uint32_t nstages;              // ring depth (stages of sw docs)
+    uint32_t nslots;               // A / D slots in TMEM (2 or kSlots)
+    uint32_t dbg;                  // debugging/timing experiments (RBE_DBG): 1 = epilogue skips TMEM loads,
+                                   // 2 = expand skips TMEM stores (results invalid)
+    int32_t f16max;                // F <= f16max - c_q for every pair: the low 16 bits keep the sign of any
+                                   // F >= 0 when c_q <= 32767 - f16max (pack::16b epilogue); 0 = never
     uint32_t sw;                   // strip width in logical threads (128 or 256) = docs per stage
     uint32_t ptop;                 // probe: values kept per (query, strip)
     uint32_t q0, nq;               // query range of this pass
@@ -105,7 +112,7 @@ struct TensorParams {
     const double* delta_h;         // [Q] histogram bin width (score units)
     const double* theta0;          // [Q] probe theta (bin 0 lower edge)
     uint64_t n;                    // top-n
-    unsigned long long* prof;      // optional [grid][kMaxWG][8] phase cycle counters (RBE_PROF=1)
+    unsigned long long* prof;      // optional [grid][8] phase cycle counters (RBE_PROF=1)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -170,6 +177,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// AND of a predicate over the 256 epilogue threads (named barrier 8 with .red.and)
+__device__ __forceinline__ bool __syncthreads_and_named(bool pred) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, 8, 256, p;\n\tselp.u32 %0, 1, 0, q;\n}"
+        : "=r"(r)
+        : "r"(uint32_t(pred))
+        : "memory");
+    return r != 0;
+}
 
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
@@ -204,6 +221,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t* v) {
         : "r"(taddr)
         : "memory");
 }
+// 64 columns, the low 16 bits of columns 2r and 2r+1 packed into register r
+__device__ __forceinline__ void tmem_ld32_p16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t* v) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -221,6 +250,33 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+// Executed by a whole warp with warp-uniform operands (kept in uniform registers); one
+// elected lane issues.  Issuing from a single divergent lane instead costs ~2x per MMA
+// (per-MMA R2UR/ELECT waterfalls: tools/microbench/mma_issue.cu).
+__device__ __forceinline__ void mma_i8_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+// one sub-tile: NKB data K blocks + the X block, accumulating into d
+template <int NKB>
+__device__ __forceinline__ void mma_group(uint32_t d, uint32_t a, uint64_t b0, uint64_t b_step, uint64_t xd,
+                                          uint32_t idesc) {
+#pragma unroll
+    for (int kb = 0; kb < NKB; ++kb) mma_i8_elect(d, a + 8 * kb, b0 + kb * b_step, idesc, kb > 0);
+    mma_i8_elect(d, a + 8 * NKB, xd, idesc, 1);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -359,7 +415,7 @@ struct RingPos {
 };
 
 struct SmemLayout {
-    size_t b, state, cqueue, qconst, bars, total;
+    size_t b, xb, state, cqueue, touched, qconst, bars, total;
 };
 
 __host__ __device__ inline size_t stage_bytes_of(uint32_t kp, uint32_t w32, uint32_t sw) {
@@ -371,102 +427,115 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uin
     auto al = [](size_t x) { return (x + 127) & ~size_t(127); };
     SmemLayout s{};
     size_t off = al(size_t(nstages) * stage_bytes_of(kp, w32, sw));
-    s.b = off;
-    off = al(off + size_t(n_pad) * 32 * (w32 + 1));
+    s.b = off;  // data K blocks of the query operand
+    off = al(off + size_t(n_pad) * 32 * w32);
+    s.xb = off;  // two X blocks (threshold), indexed by strip parity
+    off = al(off + 2 * size_t(n_pad) * 32);
     s.state = off;
-    off = al(off + size_t(kQPass) * sw * (probe ? 4 : 8));
-    s.cqueue = off;
+    off = al(off + size_t(kQPass) * sw * 4);
+    s.cqueue = off;  // also the strip end's histogram / counters scratch
     off = al(off + (probe ? 0 : size_t(kCandQueue) * 8));
+    s.touched = off;
+    off = al(off + (probe ? 0 : size_t(kQPass) * sw * 2));
     s.qconst = off;
-    off = al(off + kQPass * 8 + kQPass * 4 * 4);
+    off = al(off + kQPass * 8 + kQPass * 4 + 2 * 3 * kQPass * 4 + 16);
     s.bars = off;
-    off = al(off + (2 * nstages + 2 * kMaxWG) * 8 + 16);
+    off = al(off + (2 * nstages + 4 * kSlots + 4) * 8 + 32);
     s.total = off;
     return s;
 }
 
-// One passing pair (F >= 0): recover acc exactly, score it in FP64 and merge it
-// into the per-(query, logical thread) state under (score desc, slot asc)
-// (BoundedQueue::insert, search.cpp:32-48).  Entries hold key = (i << 32 | acc);
-// the order is independent of insertion order, so warpgroups may update the
-// same entry concurrently (64-bit CAS).
+// One passing pair (F >= 0): score it in FP64 and merge it into the
+// per-(query, logical thread) state under (score desc, slot asc)
+// (BoundedQueue::insert, search.cpp:32-48).  Entries hold key = (i << 23) |
+// (acc & 0x7fffff); the order is independent of insertion order, so threads may
+// update the same entry concurrently (CAS).
+__device__ __forceinline__ uint32_t key_i(uint32_t key) { return key >> 23; }
+__device__ __forceinline__ int32_t key_acc(uint32_t key) { return int32_t(key << 9) >> 9; }
 __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, uint32_t i, uint32_t col, uint32_t sw,
-                                            const double* theta_s, unsigned long long* st_key, const float* mags_y,
-                                            uint32_t tpb, int L) {
+                                            const double* theta_s, uint32_t* st_key, const float* mags_y,
+                                            uint32_t tpb, int L, uint16_t* touched, uint32_t* tcount) {
     const double sc = __ddiv_rn(ldexp(double(a), -L), double(mag));
     if (!(sc >= theta_s[q])) return;
-    const unsigned long long mine = (uint64_t(i) << 32) | uint32_t(a);
-    unsigned long long* ent = st_key + q * sw + col;
-    unsigned long long cur = *ent;
+    const uint32_t mine = (i << 23) | (uint32_t(a) & 0x7fffffu);
+    uint32_t* ent = st_key + q * sw + col;
+    uint32_t cur = *ent;
     while (true) {
         if (cur != kEmptyKey) {
-            const uint32_t ci = uint32_t(cur >> 32);
+            const uint32_t ci = key_i(cur);
             const double cm = double(__ldg(mags_y + uint64_t(ci) * tpb));
-            const double cs = __ddiv_rn(ldexp(double(int32_t(uint32_t(cur))), -L), cm);
+            const double cs = __ddiv_rn(ldexp(double(key_acc(cur)), -L), cm);
             if (!(sc > cs || (sc == cs && i < ci))) break;  // the current entry ranks first
         }
-        const unsigned long long prev = atomicCAS(ent, cur, mine);
-        if (prev == cur) break;
+        const uint32_t prev = atomicCAS(ent, cur, mine);
+        if (prev == cur) {
+            if (cur == kEmptyKey) touched[atomicAdd(tcount, 1u)] = uint16_t(q * sw + col);  // first entry
+            break;
+        }
         cur = prev;
     }
 }
 
-// phase timing of the worker loop (build with -DRBE_PHASE_PROF and run with RBE_PROF=1)
+// phase timing of the epilogue loop (build with -DRBE_PHASE_PROF and run with RBE_PROF=1)
 #ifdef RBE_PHASE_PROF
 #define RBE_CLK(x) const long long x = clock64()
-#define RBE_CLK_DECL(x) long long x = 0
-#define RBE_CLK_SET(x) x = clock64()
-#define RBE_CLK_COPY(x, y) x = y
 #else
 #define RBE_CLK(x)
-#define RBE_CLK_DECL(x)
-#define RBE_CLK_SET(x)
-#define RBE_CLK_COPY(x, y)
 #endif
 
+// Warp roles (20 warps, 96 registers each):
+//   warps 0-7    expand: group e = warp/4 takes sub-tiles u = e (mod 2); quadrant warp%4
+//   warps 8-15   epilogue: group e = (warp-8)/4 takes sub-tiles u = e (mod 2)
+//   warp 16      producer (ring of stages; TMEM allocator)
+//   warps 17-19  MMA issuers: warp 17+m takes sub-tiles u = m (mod 3)
+// Sub-tile u (128 docs, CTA-local counter) uses A slot u % kSlots and D slot u % kSlots.
 template <int KP, bool RW, bool PROBE>
-__global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParams p) {
+__global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t w32 = p.w32;
-    const uint32_t nwg = p.nwg;
-    const uint32_t n_workers = 128 * nwg;
     const uint32_t nst = p.nstages;
-    const uint32_t sw = p.sw;                              // strip width (logical threads): 128 or 256
-    const uint32_t spt = sw / 128;                         // 128-doc sub-tiles per stage
-    const uint32_t plane_bytes = sw * w32 * 4;             // one plane of a stage (sw docs)
+    const uint32_t sw = p.sw;                                // strip width (logical threads): 128 or 256
+    const uint32_t spt = sw / 128;                           // 128-doc sub-tiles per stage
+    const uint32_t plane_bytes = sw * w32 * 4;               // one plane of a stage (sw docs)
     const uint32_t stage_bytes = KP * plane_bytes + sw * 4;  // + the stage's f32 magnitudes
-    const uint32_t n_kb = w32 + 1;                         // data K blocks + the X block
     SmemLayout sl = smem_layout(KP, w32, p.n_pad, nst, sw, PROBE);
     uint8_t* ring = smem;
     uint8_t* bsm = smem + sl.b;
-    unsigned long long* st_key = reinterpret_cast<unsigned long long*>(smem + sl.state);  // [64][sw]
+    uint8_t* xsm = smem + sl.xb;  // [2][n_pad * 32]
+    uint32_t* st_key = reinterpret_cast<uint32_t*>(smem + sl.state);  // [64][sw]
     float* pmax = reinterpret_cast<float*>(smem + sl.state);                              // probe: [64][sw]
     uint2* cqueue = reinterpret_cast<uint2*>(smem + sl.cqueue);     // deferred candidates
     double* theta_s = reinterpret_cast<double*>(smem + sl.qconst);  // [64]
     int32_t* cq_s = reinterpret_cast<int32_t*>(theta_s + kQPass);   // [64]
-    int32_t* xc_s = cq_s + kQPass;                                  // [64] X coefficients
-    int32_t* xe_s = xc_s + kQPass;
-    int32_t* xg_s = xe_s + kQPass;
+    int32_t* xcoef = cq_s + kQPass;                                 // [2][3][64]: c, e, g per strip parity
+    uint32_t* p16ok = reinterpret_cast<uint32_t*>(xcoef + 2 * 3 * kQPass);  // [2] packed epilogue safe
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sl.bars);
-    uint64_t* full = bars;                 // [nst]  ring slot loaded (tx bytes)
-    uint64_t* empty = full + nst;          // [nst]  ring slot consumed (128 arrivals per sub-tile)
-    uint64_t* a_full = empty + nst;        // [nwg]  A complete and D free (4 warp arrivals)
-    uint64_t* mma_done = a_full + kMaxWG;  // [nwg]  MMA committed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + kMaxWG);
+    uint64_t* full = bars;                  // [nst]    stage loaded (tx bytes)
+    uint64_t* empty = full + nst;           // [nst]    stage consumed (4 warp arrivals per sub-tile)
+    uint64_t* a_full = empty + nst;         // [kSlots] A written (4 expand warps)
+    uint64_t* a_free = a_full + kSlots;     // [kSlots] MMA done reading A (commit)
+    uint64_t* d_full = a_free + kSlots;     // [kSlots] D ready (commit)
+    uint64_t* d_free = d_full + kSlots;     // [kSlots] D read (4 epilogue warps)
+    uint64_t* x_ready = d_free + kSlots;    // [2]      X block of parity b rewritten (refresher)
+    uint64_t* emitted = x_ready + 2;        // [2]      strip of parity b emitted (epilogue)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(emitted + 2);
     uint32_t* cq_count = tmem_slot + 1;
+    uint32_t* tcount = tmem_slot + 2;
+    uint16_t* touched = reinterpret_cast<uint16_t*>(smem + sl.touched);  // [64 * sw] state entries set in the strip
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int producer_warp = int(4 * nwg);
-    const int mma_warp0 = producer_warp + 1;  // nwg MMA issuer warps follow the producer
-    const uint32_t a_cols = 8 * n_kb;  // TMEM columns of one sub-tile's A (4 K bytes per column)
-    const uint32_t d_cols = p.n_pad;   // TMEM columns of one sub-tile's D
+    const uint32_t a_cols = 8 * (w32 + 1);  // TMEM columns of one A (4 K bytes per column)
+    const uint32_t d_cols = p.n_pad;        // TMEM columns of one D
     uint32_t tmem_cols = 32;
-    while (tmem_cols < nwg * (2 * a_cols + d_cols)) tmem_cols <<= 1;
+    const uint32_t nsl = p.nslots;                  // 2 or 4
+    const uint32_t nsl_sh = nsl == 4 ? 2 : 1;
+    const uint32_t spt_sh = spt == 2 ? 1 : 0;
+    while (tmem_cols < nsl * (a_cols + d_cols)) tmem_cols <<= 1;
     const int L = int(p.L);
     const double lam = double(1u << p.lam_shift);
 
-    // ---- one-time setup: B image (data blocks from global, X block per query)
+    // ---- one-time setup: B image (data blocks from global, both X blocks from theta)
     for (uint32_t e = threadIdx.x; e < p.n_pad * 32 * w32 / 16; e += blockDim.x)
         reinterpret_cast<uint4*>(bsm)[e] = reinterpret_cast<const uint4*>(p.bimg)[e];
     for (uint32_t q = threadIdx.x; q < kQPass; q += blockDim.x) {
@@ -476,11 +545,17 @@ __global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParam
         XCoef x;
         if (PROBE) x = live ? XCoef{int32_t(cq_s[q] * int32_t(1u << p.lam_shift)), 0, 0} : XCoef{-kXMax, 0, 0};
         else x = x_coeffs(theta_s[q], cq_s[q], L, lam, p.m0, p.delta, p.mmax);
-        xc_s[q] = x.c;
-        xe_s[q] = x.e;
-        xg_s[q] = x.g;
-        write_xrow(bsm, p.n_pad, w32, q, x);
+        for (int b = 0; b < 2; ++b) {
+            xcoef[(b * 3 + 0) * kQPass + q] = x.c;
+            xcoef[(b * 3 + 1) * kQPass + q] = x.e;
+            xcoef[(b * 3 + 2) * kQPass + q] = x.g;
+            write_xrow(xsm + b * p.n_pad * 32, p.n_pad, 0, q, x);
+        }
     }
+    if (threadIdx.x < 2) p16ok[threadIdx.x] = 1u;
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < p.nq; q += blockDim.x)
+        if (p.f16max == 0 || xcoef[q] > 32767 - p.f16max) p16ok[0] = p16ok[1] = 0u;
     for (uint32_t e = threadIdx.x; e < kQPass * sw; e += blockDim.x) {
         if (PROBE) pmax[e] = -INFINITY;
         else st_key[e] = kEmptyKey;
@@ -488,16 +563,23 @@ __global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParam
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < nst; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 128 * spt);
+            mbar_init(empty + s, 4 * spt);
         }
-        for (uint32_t w = 0; w < nwg; ++w) {
-            mbar_init(a_full + w, 4);
-            mbar_init(mma_done + w, 1);
+        for (int k = 0; k < kSlots; ++k) {
+            mbar_init(a_full + k, 4);
+            mbar_init(a_free + k, 1);
+            mbar_init(d_full + k, 1);
+            mbar_init(d_free + k, 4);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(x_ready + b, 1);
+            mbar_init(emitted + b, 1);
         }
         *cq_count = 0;
+        *tcount = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == producer_warp) {
+    if (warp == kProducerWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -508,25 +590,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParam
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    auto a_addr = [&](uint32_t slot) { return tmem_base + slot * a_cols; };
+    auto d_addr = [&](uint32_t slot) { return tmem_base + nsl * a_cols + slot * d_cols; };
 
-    if (warp == producer_warp) {
-        // ===================== producer: one contiguous sw-doc stage per tile of the strip =====================
+    if (warp == kProducerWarp) {
+        // ===================== producer: one contiguous sw-doc stage per tile of each strip =====================
         if (lane == 0) {
             RingPos rs;
-#ifdef RBE_PHASE_PROF
-            long long t_wait = 0, t_start = clock64();
-#endif
             for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
                 const StripInfo si = strip_info(p, s);
                 const PartDesc& part = p.parts[si.part];
                 for (uint32_t i = 0; i < si.n_tiles; ++i, rs.next(nst)) {
-#ifdef RBE_PHASE_PROF
-                    const long long tw = clock64();
-#endif
                     mbar_wait_sleep(empty + rs.idx, rs.phase ^ 1);
-#ifdef RBE_PHASE_PROF
-                    t_wait += clock64() - tw;
-#endif
                     mbar_expect_tx(full + rs.idx, stage_bytes);
                     const uint64_t slot0 = si.base + uint64_t(i) * p.tpb;
                     uint8_t* dst = ring + rs.idx * stage_bytes;
@@ -537,276 +612,353 @@ __global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParam
                     bulk_g2s(dst + KP * plane_bytes, part.mags + slot0, sw * 4, full + rs.idx);
                 }
             }
-#ifdef RBE_PHASE_PROF
-            if (p.prof) {
-                p.prof[(uint64_t(blockIdx.x) * kMaxWG) * 8 + 6] += t_wait;
-                p.prof[(uint64_t(blockIdx.x) * kMaxWG) * 8 + 7] += clock64() - t_start;
-            }
-#endif
         }
-    } else if (warp >= mma_warp0 && warp < mma_warp0 + int(nwg)) {
-        // ===================== MMA issuers: one warp per warpgroup, its sub-tiles in order =====================
-        const uint32_t w = uint32_t(warp - mma_warp0);
-        if (lane == 0) {
+    } else if (warp >= kMmaWarp0 && warp < kMmaWarp0 + kMmaWarps) {
+        // ===================== MMA issuers: sub-tiles u = m (mod 2) in order =====================
+        const uint32_t m = uint32_t(warp - kMmaWarp0);
+        {
+            // the whole warp runs this loop (operands stay warp-uniform); one lane issues
             const uint32_t idesc = idesc_i8(128, p.n_pad);
             const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
+            const uint64_t x_desc0 = smem_desc(smem_u32(xsm));
             const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
-            const uint32_t a_base = tmem_base + w * (2 * a_cols + d_cols);
-            const uint32_t d_t = a_base + 2 * a_cols;
-            uint32_t c = 0, u0 = 0;
-            for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
+            uint32_t u0 = 0, sidx = 0;
+            for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
                 const StripInfo si = strip_info(p, s);
                 const uint32_t n_sub = si.n_tiles * spt;
-                // this warpgroup's sub-tiles of the strip: k = first, first + nwg, ...
-                const uint32_t first = (w + nwg - u0 % nwg) % nwg;
-                const uint32_t mine = n_sub > first ? (n_sub - first + nwg - 1) / nwg : 0;
-                u0 += n_sub;
-                for (uint32_t k = 0; k < mine; ++k, ++c) {
-                    mbar_wait_sleep(a_full + w, c & 1);
+                if (!PROBE && sidx >= 2 && n_sub > 0) {
+                    // X block of parity sidx&1 was rewritten at the end of strip sidx-2
+                    mbar_wait_sleep(x_ready + (sidx & 1), ((sidx - 2) >> 1) & 1);
+                }
+                const uint64_t xd = x_desc0 + (sidx & 1) * b_step;
+                // warp m issues the sub-tiles of slots = m (mod kMmaWarps): each of its
+                // barriers is visited at every use, so parity waits are unambiguous
+                for (uint32_t k = (m + kMmaWarps - u0 % kMmaWarps) % kMmaWarps; k < n_sub; k += kMmaWarps) {
+                    const uint32_t u = u0 + k, slot = u & (nsl - 1), use = u >> nsl_sh;
+#ifdef RBE_PHASE_PROF
+                    const long long m0c = clock64();
+#endif
+                    mbar_wait_sleep(a_full + slot, use & 1);
+#ifdef RBE_PHASE_PROF
+                    const long long m1c = clock64();
+#endif
+                    mbar_wait_sleep(d_free + slot, (use & 1) ^ 1);
+#ifdef RBE_PHASE_PROF
+                    const long long m2c = clock64();
+                    if (p.prof && m == 0 && lane == 0) {
+                        p.prof[uint64_t(1024 + blockIdx.x) * 8 + 0] += m1c - m0c;
+                        p.prof[uint64_t(1024 + blockIdx.x) * 8 + 1] += m2c - m1c;
+                        p.prof[uint64_t(1024 + blockIdx.x) * 8 + 5] += 1;
+                    }
+#endif
                     tc_fence_after();
-                    const uint32_t a_t = a_base + (c & 1) * a_cols;
-                    uint64_t bd = b_desc0;
-                    for (uint32_t kb = 0; kb < n_kb; ++kb, bd += b_step) mma_i8(d_t, a_t + 8 * kb, bd, idesc, kb > 0);
-                    mma_commit(mma_done + w);
+                    const uint32_t a_t = a_addr(slot), d_t = d_addr(slot);
+                    switch (w32) {
+                        case 2: mma_group<2>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                        case 4: mma_group<4>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                        case 6: mma_group<6>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                        default: mma_group<8>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                    }
+                    mma_commit_elect(d_full + slot);  // D ready and A free (expand waits on it too)
+                    __syncwarp();
+#ifdef RBE_PHASE_PROF
+                    if (p.prof && m == 0 && lane == 0) p.prof[uint64_t(1024 + blockIdx.x) * 8 + 2] += clock64() - m2c;
+#endif
                 }
+                u0 += n_sub;
             }
         }
-    } else {
-        // ===================== workers: warpgroup wg handles sub-tiles u = wg (mod nwg) =====================
-        // Per warpgroup, software-pipelined within a strip:
-        //   expand(k+1) -> A[(k+1)&1]  while the tensor core runs MMA(k) from A[k&1]
-        //   wait MMA(k); test D; arrive a_full (A(k+1) ready, D free) -> the MMA warp issues MMA(k+1)
-        const uint32_t wg = uint32_t(warp >> 2);
+    } else if (warp < 8) {
+        // ===================== expand warps =====================
+        const uint32_t e = uint32_t(warp >> 2);
         const int quad = warp & 3;
-        const uint32_t l = uint32_t(quad * 32 + lane);  // TMEM lane == doc within the sub-tile
-        const uint32_t wt = uint32_t(threadIdx.x);      // worker thread id
+        const uint32_t l = uint32_t(quad * 32 + lane);
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        const uint32_t a_t0 = tmem_base + wg * (2 * a_cols + d_cols);  // this warpgroup's A[0], A[1]
-        const uint32_t d_t = a_t0 + 2 * a_cols + lane_base;            // and D (this warp's lanes)
-        const uint32_t w64 = w32 / 2;
-        const uint32_t n_worker_warps = 4 * nwg;
-        const uint32_t pstride = p.ptop;
-        uint32_t scored = 0, cands = 0;
-        uint32_t kc = 0;  // sub-tiles processed by this warpgroup (A buffer / barrier parities)
-        float pm[PROBE ? kQPass : 1];
-#pragma unroll
-        for (int e = 0; e < (PROBE ? kQPass : 1); ++e) pm[e] = -INFINITY;
         {
-            // constant columns 2..7 of the X block of both A buffers (K bytes 8..31 = 255)
+            // constant columns 2..7 of the X block of every A slot (K bytes 8..31 = 255)
             uint32_t v[8] = {0u, 0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u};
-            tmem_st8(a_t0 + lane_base + 8 * w32, v);
-            tmem_st8(a_t0 + a_cols + lane_base + 8 * w32, v);
+            for (uint32_t k = e; k < nsl; k += 2) tmem_st8(a_addr(k) + lane_base + 8 * w32, v);
             tmem_wait_st();
         }
-
-        // expand doc `col` of ring stage `st` into A buffer `ab`; returns its magnitude and bin
-        auto expand = [&](uint32_t st, uint32_t col, uint32_t ab, float& mag, uint32_t& j) {
-            const uint8_t* stage = ring + st * stage_bytes;
-            const uint32_t a_t = a_t0 + ab * a_cols + lane_base;
-            if ((w32 & 3) == 0) {
-                // 16-byte loads: a warp reads 32 consecutive docs x 16 B = 512 B, conflict-free
-                const uint4* src = reinterpret_cast<const uint4*>(stage);
-                const uint32_t w128 = w32 / 4;
-                for (uint32_t g4 = 0; g4 < w128; ++g4) {
-                    uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
-#pragma unroll
-                    for (int t = 0; t < KP; ++t) {
-                        const uint4 v = src[(t * sw + col) * w128 + g4];
-                        w0[t] = v.x;
-                        w1[t] = v.y;
-                        w2[t] = v.z;
-                        w3[t] = v.w;
-                    }
-                    uint32_t out[16];
-                    Expand<KP, RW>::run(w0, out);
-                    Expand<KP, RW>::run(w1, out + 8);
-                    tmem_st16(a_t + 32 * g4, out);
-                    Expand<KP, RW>::run(w2, out);
-                    Expand<KP, RW>::run(w3, out + 8);
-                    tmem_st16(a_t + 32 * g4 + 16, out);
-                }
-            } else {
-                const uint2* src = reinterpret_cast<const uint2*>(stage);
-                for (uint32_t g2 = 0; g2 < w64; ++g2) {
-                    uint32_t w0[KP], w1[KP];
-#pragma unroll
-                    for (int t = 0; t < KP; ++t) {
-                        const uint2 v = src[(t * sw + col) * w64 + g2];
-                        w0[t] = v.x;
-                        w1[t] = v.y;
-                    }
-                    uint32_t out[16];
-                    Expand<KP, RW>::run(w0, out);
-                    Expand<KP, RW>::run(w1, out + 8);
-                    tmem_st16(a_t + 16 * g2, out);
-                }
-            }
-            mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
-            j = mag_bin(mag, p.m0f, p.inv_df);
-            tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
-            mbar_arrive(empty + st);  // this sub-tile's share of the ring slot is consumed
-        };
-        // this warp's part of A is complete and its D reads are done: one arrival per warp
-        auto arrive_a = [&]() {
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(a_full + wg);
-        };
-
-        uint32_t u0 = 0;       // sub-tiles of earlier strips (this CTA)
-        uint32_t tiles0 = 0;   // ring stages (tiles) of earlier strips (this CTA)
+#ifdef RBE_PHASE_PROF
+        long long x_wait = 0, x_work = 0;
+#endif
+        uint32_t u0 = 0, tiles0 = 0;
         for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
             const StripInfo si = strip_info(p, s);
-            const PartDesc& part = p.parts[si.part];
             const uint32_t n_sub = si.n_tiles * spt;
-            const uint64_t lim = part.count > si.base ? part.count - si.base : 0;  // valid: i*tpb + col < lim
-            // this warpgroup's sub-tiles k = first, first + nwg, ... (u = u0 + k, u % nwg == wg)
-            uint32_t k = (wg + nwg - u0 % nwg) % nwg;
+            uint32_t k = (e + 2 - (u0 & 1)) & 1;
             if (k < n_sub) {
-                // ring position of the tile holding sub-tile k, advanced incrementally
                 uint32_t ti = k / spt;
                 uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
-                auto seek = [&](uint32_t t_new) {
-                    for (; ti < t_new; ++ti)
+                for (; k < n_sub; k += 2) {
+                    for (const uint32_t tn = k >> spt_sh; ti < tn; ++ti)
                         if (++st_idx == nst) {
                             st_idx = 0;
                             st_ph ^= 1;
                         }
-                };
-                RBE_CLK_DECL(c1);
-                float mag, mag_n = 0.0f;
-                uint32_t j, j_n = 0;
-                uint32_t col = (k % spt) * 128 + l, col_n = 0;
-                mbar_wait(full + st_idx, st_ph);
-                expand(st_idx, col, kc & 1, mag, j);
-                arrive_a();
-                while (true) {
-                    const uint32_t k_n = k + nwg;
-                    const bool has_next = k_n < n_sub;
-                    const uint32_t i = k / spt;
-                    RBE_CLK(c0);
-                    if (has_next) {
-                        seek(k_n / spt);
-                        col_n = (k_n % spt) * 128 + l;
-                        mbar_wait(full + st_idx, st_ph);
-                        RBE_CLK_SET(c1);
-                        expand(st_idx, col_n, (kc + 1) & 1, mag_n, j_n);
-                    } else {
-                        RBE_CLK_COPY(c1, c0);
-                    }
-                    RBE_CLK(c2);
-                    const bool valid = uint64_t(i) * p.tpb + col < lim;
-                    scored += valid ? 1 : 0;
-                    mbar_wait_sleep(mma_done + wg, kc & 1);
+                    const uint32_t u = u0 + k, slot = u & (nsl - 1), use = u >> nsl_sh;
+                    const uint32_t col = (k & (spt - 1)) * 128 + l;
+#ifdef RBE_PHASE_PROF
+                    const long long tw0 = clock64();
+#endif
+                    mbar_wait_sleep(full + st_idx, st_ph);
+                    mbar_wait_sleep(d_full + slot, (use & 1) ^ 1);  // MMA(u - nsl) done: A slot free
+#ifdef RBE_PHASE_PROF
+                    const long long tw1 = clock64();
+                    x_wait += tw1 - tw0;
+#endif
                     tc_fence_after();
-                    RBE_CLK(c3);
-                    if (PROBE) {
-                        // F = lambda acc; per-thread maxima of the (float) score
-                        const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
+                    const uint8_t* stage = ring + st_idx * stage_bytes;
+                    const uint32_t a_t = a_addr(slot) + lane_base;
+                    if ((w32 & 3) == 0) {
+                        // 16-byte loads: a warp reads 32 consecutive docs x 16 B = 512 B, conflict-free
+                        const uint4* src = reinterpret_cast<const uint4*>(stage);
+                        const uint32_t w128 = w32 / 4;
+                        for (uint32_t g4 = 0; g4 < w128; ++g4) {
+                            uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
 #pragma unroll
-                        for (int c = 0; c < kQPass / 16; ++c) {
-                            int32_t F[16];
-                            tmem_ld16(d_t + 16 * c, F);
-                            tmem_wait_ld();
-                            if (valid) {
-#pragma unroll
-                                for (int e = 0; e < 16; ++e)
-                                    pm[16 * c + e] = fmaxf(pm[16 * c + e], float(F[e]) * scale);
+                            for (int t = 0; t < KP; ++t) {
+                                const uint4 v = src[(t * sw + col) * w128 + g4];
+                                w0[t] = v.x;
+                                w1[t] = v.y;
+                                w2[t] = v.z;
+                                w3[t] = v.w;
+                            }
+                            uint32_t out[16];
+                            Expand<KP, RW>::run(w0, out);
+                            Expand<KP, RW>::run(w1, out + 8);
+                            if (p.dbg & 2) {
+                                if (out[0] == 0x12345678u) tmem_st16(a_t + 32 * g4, out);
+                            } else {
+                                tmem_st16(a_t + 32 * g4, out);
+                            }
+                            Expand<KP, RW>::run(w2, out);
+                            Expand<KP, RW>::run(w3, out + 8);
+                            if (p.dbg & 2) {
+                                if (out[0] == 0x12345678u) tmem_st16(a_t + 32 * g4 + 16, out);
+                            } else {
+                                tmem_st16(a_t + 32 * g4 + 16, out);
                             }
                         }
                     } else {
-                        // F >= 0 is necessary for score >= theta: AND the sign bits, 32 queries
-                        // at a time; the rare passing groups are re-read from TMEM
-                        uint32_t gmask = 0;  // bit g: some F >= 0 among queries [8g, 8g+8)
+                        const uint2* src = reinterpret_cast<const uint2*>(stage);
+                        const uint32_t w64 = w32 / 2;
+                        for (uint32_t g2 = 0; g2 < w64; ++g2) {
+                            uint32_t w0[KP], w1[KP];
 #pragma unroll
-                        for (int h = 0; h < kQPass / 32; ++h) {
-                            int32_t F[32];
-                            tmem_ld32(d_t + 32 * h, F);
+                            for (int t = 0; t < KP; ++t) {
+                                const uint2 v = src[(t * sw + col) * w64 + g2];
+                                w0[t] = v.x;
+                                w1[t] = v.y;
+                            }
+                            uint32_t out[16];
+                            Expand<KP, RW>::run(w0, out);
+                            Expand<KP, RW>::run(w1, out + 8);
+                            tmem_st16(a_t + 16 * g2, out);
+                        }
+                    }
+                    const float mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
+                    const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
+                    tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(a_full + slot);
+#ifdef RBE_PHASE_PROF
+                    x_work += clock64() - tw1;
+#endif
+                }
+            }
+            u0 += n_sub;
+            tiles0 += si.n_tiles;
+        }
+#ifdef RBE_PHASE_PROF
+        if (p.prof && lane == 0 && warp == 1) {
+            p.prof[uint64_t(blockIdx.x) * 8 + 3] += x_wait;
+            p.prof[uint64_t(blockIdx.x) * 8 + 4] += x_work;
+        }
+#endif
+    } else if (warp < 16) {
+        // ===================== epilogue warps =====================
+        const uint32_t e = uint32_t((warp - 8) >> 2);
+        const int quad = warp & 3;
+        const uint32_t l = uint32_t(quad * 32 + lane);
+        const uint32_t lane_base = uint32_t(quad * 32) << 16;
+        const uint32_t et = uint32_t(threadIdx.x - 256);  // epilogue thread id [0, 256)
+        const uint32_t pstride = p.ptop;
+        uint32_t scored = 0, cands = 0;
+        float pm[PROBE ? kQPass : 1];
+#pragma unroll
+        for (int k2 = 0; k2 < (PROBE ? kQPass : 1); ++k2) pm[k2] = -INFINITY;
+#ifdef RBE_PHASE_PROF
+        long long t_wait = 0, t_work = 0, t_end = 0, t_ld = 0, t_red = 0;
+#endif
+        uint32_t u0 = 0, tiles0 = 0, sidx = 0;
+        for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
+            const StripInfo si = strip_info(p, s);
+            const PartDesc& part = p.parts[si.part];
+            const uint32_t n_sub = si.n_tiles * spt;
+            const uint64_t lim = part.count > si.base ? part.count - si.base : 0;  // valid: i*tpb + col < lim
+            if (!PROBE && sidx >= 2 && n_sub > 0) mbar_wait_sleep(x_ready + (sidx & 1), ((sidx - 2) >> 1) & 1);
+            const int32_t* xc = xcoef + (sidx & 1) * 3 * kQPass;
+            const bool p16 = p16ok[sidx & 1] != 0;
+            uint32_t k = (e + 2 - (u0 & 1)) & 1;
+            uint32_t ti = k >> spt_sh;
+            uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
+            for (; k < n_sub; k += 2) {
+                for (const uint32_t tn = k >> spt_sh; ti < tn; ++ti)
+                    if (++st_idx == nst) {
+                        st_idx = 0;
+                        st_ph ^= 1;
+                    }
+                const uint32_t u = u0 + k, slot = u & (nsl - 1), use = u >> nsl_sh;
+                const uint32_t i = k >> spt_sh, col = (k & (spt - 1)) * 128 + l;
+                const bool valid = uint64_t(i) * p.tpb + col < lim;
+                const float* stage_mags = reinterpret_cast<const float*>(ring + st_idx * stage_bytes + KP * plane_bytes);
+                scored += valid ? 1 : 0;
+                RBE_CLK(c0);
+                mbar_wait_sleep(d_full + slot, use & 1);
+                tc_fence_after();
+                RBE_CLK(c1);
+                const uint32_t d_t = d_addr(slot) + lane_base;
+                if (PROBE) {
+                    // F = lambda acc; per-thread maxima of the (float) score
+                    mbar_wait(full + st_idx, st_ph);  // complete: the stage is held until our arrival
+                    const float mag = stage_mags[col];
+                    const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
+#pragma unroll
+                    for (int c = 0; c < kQPass / 16; ++c) {
+                        int32_t F[16];
+                        tmem_ld16(d_t + 16 * c, F);
+                        tmem_wait_ld();
+                        if (valid) {
+#pragma unroll
+                            for (int e2 = 0; e2 < 16; ++e2)
+                                pm[16 * c + e2] = fmaxf(pm[16 * c + e2], float(F[e2]) * scale);
+                        }
+                    }
+                } else {
+                    // F >= 0 is necessary for score >= theta: AND the sign bits per group of 8
+                    uint32_t gmask = 0;  // bit g: some F >= 0 among queries [8g, 8g+8)
+                    if (p16) {
+                        // low 16 bits of all 64 accumulators in 32 registers (pack::16b); the
+                        // sign of every F >= 0 survives, a wrapped F < 0 is rejected exactly below
+                        uint32_t R[32];
+                        if (p.dbg & 1) {
+#pragma unroll
+                            for (int e2 = 0; e2 < 32; ++e2) R[e2] = 0x80008000u;
+                        } else {
+                            tmem_ld32_p16(d_t, R);
                             tmem_wait_ld();
+                        }
+#ifdef RBE_PHASE_PROF
+                        t_ld += clock64() - c1;
+#endif
+                        uint32_t a4[4];
 #pragma unroll
-                            for (int g = 0; g < 4; ++g) {
-                                uint32_t a = uint32_t(F[8 * g]);
+                        for (int g = 0; g < 4; ++g) {
+                            uint32_t a = R[8 * g];
 #pragma unroll
-                                for (int e = 1; e < 8; ++e) a &= uint32_t(F[8 * g + e]);
-                                gmask |= (~a >> 31) << (4 * h + g);
+                            for (int e2 = 1; e2 < 8; ++e2) a &= R[8 * g + e2];
+                            a4[g] = a;
+                        }
+                        const uint32_t all = (a4[0] & a4[1]) & (a4[2] & a4[3]);
+                        if ((~all & 0x80008000u) && valid) {
+#pragma unroll
+                            for (int g = 0; g < kQPass / 8; ++g) {
+                                const uint32_t a = (R[4 * g] & R[4 * g + 1]) & (R[4 * g + 2] & R[4 * g + 3]);
+                                gmask |= uint32_t((~a & 0x80008000u) != 0u) << g;
                             }
                         }
-                        // groups with a passing pair in any valid lane of the warp (tcgen05.ld is
-                        // warp-collective, so the whole warp re-reads them together)
-                        uint32_t wmask = __reduce_or_sync(0xffffffffu, valid ? gmask : 0u);
+                    } else {
+                        int32_t F[kQPass];
+                        tmem_ld32(d_t, F);
+                        tmem_ld32(d_t + 32, F + 32);
+                        tmem_wait_ld();
+#ifdef RBE_PHASE_PROF
+                        t_ld += clock64() - c1;
+#endif
+#pragma unroll
+                        for (int g = 0; g < kQPass / 8; ++g) {
+                            uint32_t a = uint32_t(F[8 * g]);
+#pragma unroll
+                            for (int e2 = 1; e2 < 8; ++e2) a &= uint32_t(F[8 * g + e2]);
+                            gmask |= (~a >> 31) << g;
+                        }
+                    }
+                    if (!valid) gmask = 0;
+#ifdef RBE_PHASE_PROF
+                    t_red += clock64() - c1;
+#endif
+                    // groups with a passing pair in any lane (tcgen05.ld is warp-collective)
+                    uint32_t wmask = __reduce_or_sync(0xffffffffu, gmask);
+                    if (wmask) {
+                        // rare: re-read those groups and queue each passing pair for exact FP64
+                        // scoring at the strip end
+                        mbar_wait(full + st_idx, st_ph);  // complete: the stage is held until our arrival
+                        const float mag = stage_mags[col];
+                        const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
                         while (wmask) {
-                            const int g = __ffs(wmask) - 1;
+                            const uint32_t g = uint32_t(__ffs(wmask) - 1);
                             wmask &= wmask - 1;
                             int32_t v[8];
                             tmem_ld8(d_t + 8 * g, v);
                             tmem_wait_ld();
-                            if (!valid || !((gmask >> g) & 1)) continue;
+                            if (!((gmask >> g) & 1)) continue;
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                if (v[e] < 0) continue;
+                            for (int e2 = 0; e2 < 8; ++e2) {
+                                if (v[e2] < 0) continue;
                                 ++cands;
-                                const uint32_t q = uint32_t(8 * g + e);
-                                const int32_t X = xc_s[q] - xe_s[q] * int32_t(j) - xg_s[q] * int32_t(j >> 4);
-                                const int32_t num = v[e] - X;
+                                const uint32_t q = 8 * g + uint32_t(e2);
+                                const int32_t X = xc[q] - xc[kQPass + q] * int32_t(j) - xc[2 * kQPass + q] * int32_t(j >> 4);
+                                const int32_t num = v[e2] - X;
                                 if (num & ((1 << p.lam_shift) - 1)) atomicAdd(p.error, 1u);
                                 const int32_t a = (num >> p.lam_shift) + cq_s[q];
-                                // defer to the strip end (exact FP64 scoring in bulk); score now if full
                                 const uint32_t pos = atomicAdd(cq_count, 1u);
                                 if (pos < kCandQueue)
                                     cqueue[pos] = make_uint2((q << 26) | i, (col << 24) | (uint32_t(a) & 0xffffffu));
                                 else
-                                    take_candidate(a, q, mag, i, col, sw, theta_s, st_key,
-                                                   part.mags + si.base + col, p.tpb, L);
+                                    take_candidate(a, q, mag, i, col, sw, theta_s, st_key, part.mags + si.base + col,
+                                                   p.tpb, L, touched, tcount);
                             }
                         }
                     }
-                    RBE_CLK(c4);
-                    ++kc;
-                    if (!has_next) break;
-                    arrive_a();
-#ifdef RBE_PHASE_PROF
-                    if (p.prof && lane == 0 && quad == 1) {
-                        long long c5 = clock64();
-                        unsigned long long* pr = p.prof + (uint64_t(blockIdx.x) * kMaxWG + wg) * 8;
-                        pr[0] += c1 - c0;  // wait full
-                        pr[1] += c2 - c1;  // expand
-                        pr[2] += c3 - c2;  // wait mma
-                        pr[3] += c4 - c3;  // epilogue
-                        pr[4] += c5 - c4;  // arrive
-                        pr[5] += 1;
-                    }
-#endif
-                    k = k_n;
-                    col = col_n;
-                    mag = mag_n;
-                    j = j_n;
                 }
                 tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(d_free + slot);
+                    mbar_arrive(empty + st_idx);  // this warp's share of the stage is consumed
+                }
+#ifdef RBE_PHASE_PROF
+                RBE_CLK(c2);
+                t_wait += c1 - c0;
+                t_work += c2 - c1;
+#endif
             }
             u0 += n_sub;
             tiles0 += si.n_tiles;
-            // ================= strip end (all worker warps) =================
+            RBE_CLK(c3);
+            // ================= strip end (all 256 epilogue threads) =================
             if (PROBE) {
-                // merge the warpgroups' per-lane maxima: in the probe each warpgroup's lanes
-                // always hold the same logical threads (host: nwg == spt when spt > 1)
-                {
-                    const uint32_t colp = (wg % spt) * 128 + l;
-                    for (uint32_t w = 0; w < nwg; ++w) {
-                        if (w == wg) {
+                // merge the two groups' per-lane maxima (each group always holds the same
+                // logical threads when spt == 2; both hold column l when spt == 1)
+                const uint32_t colp = (e % spt) * 128 + l;
+                for (uint32_t w = 0; w < 2; ++w) {
+                    if (w == e) {
 #pragma unroll
-                            for (int e = 0; e < kQPass; ++e) {
-                                float* m = pmax + e * sw + colp;
-                                *m = fmaxf(*m, pm[e]);
-                                pm[e] = -INFINITY;
-                            }
+                        for (int k2 = 0; k2 < kQPass; ++k2) {
+                            float* mm = pmax + k2 * sw + colp;
+                            *mm = fmaxf(*mm, pm[k2]);
+                            pm[k2] = -INFINITY;
                         }
-                        named_bar(kAllBar, n_workers);
                     }
+                    named_bar(kEpiBar, 256);
                 }
                 // per query keep the top ptop per-thread maxima of the strip (distinct threads)
-                const uint32_t vpl = sw / 32;  // values per lane
-                for (uint32_t q = uint32_t(warp); q < p.nq; q += n_worker_warps) {
+                const uint32_t vpl = sw / 32;
+                for (uint32_t q = uint32_t(warp - 8); q < p.nq; q += 8) {
                     float v[8];
 #pragma unroll
                     for (int k2 = 0; k2 < 8; ++k2) v[k2] = uint32_t(k2) < vpl ? pmax[q * sw + 32 * k2 + lane] : -INFINITY;
@@ -814,106 +966,167 @@ __global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParam
                         float best = v[0];
 #pragma unroll
                         for (int k2 = 1; k2 < 8; ++k2) best = fmaxf(best, v[k2]);
-                        float m = best;
-                        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-                        const unsigned holder = __ballot_sync(0xffffffffu, best == m);
+                        float mx = best;
+                        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+                        const unsigned holder = __ballot_sync(0xffffffffu, best == mx);
                         if (lane == __ffs(holder) - 1) {
                             bool done = false;
 #pragma unroll
                             for (int k2 = 0; k2 < 8; ++k2)
-                                if (!done && v[k2] == m) {
+                                if (!done && v[k2] == mx) {
                                     v[k2] = -INFINITY;
                                     done = true;
                                 }
                         }
-                        if (lane == 0) p.probe_out[(uint64_t(p.q0 + q) * p.n_strips + s) * pstride + r] = m;
+                        if (lane == 0) p.probe_out[(uint64_t(p.q0 + q) * p.n_strips + s) * pstride + r] = mx;
                     }
                 }
-                named_bar(kAllBar, n_workers);
-                for (uint32_t e = wt; e < kQPass * sw; e += n_workers) pmax[e] = -INFINITY;
-                named_bar(kAllBar, n_workers);
+                named_bar(kEpiBar, 256);
+                for (uint32_t k2 = et; k2 < kQPass * sw; k2 += 256) pmax[k2] = -INFINITY;
+                named_bar(kEpiBar, 256);
                 continue;
             }
-            named_bar(kAllBar, n_workers);
-            // exact FP64 scoring of the strip's deferred candidates (all worker threads)
+            named_bar(kEpiBar, 256);
+#ifdef RBE_PHASE_PROF
+            const long long e0c = clock64();
+#endif
+            // exact FP64 scoring of the strip's deferred candidates
             {
                 const uint32_t nc = min(*cq_count, uint32_t(kCandQueue));
-                for (uint32_t e = wt; e < nc; e += n_workers) {
-                    const uint2 c = cqueue[e];
+                for (uint32_t k2 = et; k2 < nc; k2 += 256) {
+                    const uint2 c = cqueue[k2];
                     const uint32_t q = c.x >> 26, ii = c.x & 0x3ffffffu, cc = c.y >> 24;
                     const int32_t a = int32_t(c.y << 8) >> 8;
-                    const float m = __ldg(part.mags + si.base + cc + uint64_t(ii) * p.tpb);
-                    take_candidate(a, q, m, ii, cc, sw, theta_s, st_key, part.mags + si.base + cc, p.tpb, L);
+                    const float mg = __ldg(part.mags + si.base + cc + uint64_t(ii) * p.tpb);
+                    take_candidate(a, q, mg, ii, cc, sw, theta_s, st_key, part.mags + si.base + cc, p.tpb, L, touched,
+                                   tcount);
                 }
             }
-            named_bar(kAllBar, n_workers);
-            if (wt == 0) *cq_count = 0;
-            // emit the strip's survivors >= theta (one per (query, logical thread))
-            for (uint32_t e = wt; e < p.nq * sw; e += n_workers) {
-                const unsigned long long key = st_key[e];
-                if (key == kEmptyKey) continue;
-                st_key[e] = kEmptyKey;
-                const uint32_t q = e / sw, cc = e % sw;
-                const uint32_t ii = uint32_t(key >> 32);
-                const int32_t a = int32_t(uint32_t(key));
-                const uint64_t slot = si.base + cc + uint64_t(ii) * p.tpb;
-                const double sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
-                if (!(sc >= theta_s[q])) continue;  // theta may have risen since it was queued
-                const unsigned long long pos = atomicAdd(p.surv_count + p.q0 + q, 1ull);
-                if (pos < p.surv_cap) {
-                    Result r;
-                    r.score = sc;
-                    r.id = part.ids[slot];
-                    r.acc = a;
-                    r.partition = part.ordinal;
-                    r.valid = 1;
-                    p.surv[uint64_t(p.q0 + q) * p.surv_cap + pos] = r;
+            named_bar(kEpiBar, 256);
+            if (et == 0) *cq_count = 0;
+#ifdef RBE_PHASE_PROF
+            const long long e1c = clock64();
+#endif
+            // emit the strip's survivors >= theta (one per (query, logical thread)) from the
+            // list of state entries set in this strip: pass 1 counts per query, one global
+            // reservation per query, pass 2 writes; the histogram is merged in shared memory
+            {
+                uint32_t* scnt = reinterpret_cast<uint32_t*>(cqueue);       // [64] per-query counters
+                unsigned long long* sbase = reinterpret_cast<unsigned long long*>(scnt + kQPass);  // [64]
+                uint32_t* hist_s = reinterpret_cast<uint32_t*>(sbase + kQPass);  // [64][kBins]
+                const uint32_t nt = *tcount;
+                if (et < kQPass) scnt[et] = 0;
+                for (uint32_t k2 = et; k2 < kQPass * kBins; k2 += 256) hist_s[k2] = 0;
+                named_bar(kEpiBar, 256);
+                auto survivor = [&](uint32_t ent, uint32_t& q, uint64_t& slot, int32_t& a, double& sc) {
+                    const uint32_t key = st_key[ent];
+                    q = ent / sw;
+                    const uint32_t cc = ent % sw;
+                    a = key_acc(key);
+                    slot = si.base + cc + uint64_t(key_i(key)) * p.tpb;
+                    sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
+                    return sc >= theta_s[q];  // theta may have risen since the entry was set
+                };
+                for (uint32_t k2 = et; k2 < nt; k2 += 256) {
+                    uint32_t q;
+                    uint64_t slot;
+                    int32_t a;
+                    double sc;
+                    if (survivor(touched[k2], q, slot, a, sc)) atomicAdd(scnt + q, 1u);
                 }
-                // every emitted survivor is a final survivor of a distinct logical thread
-                const double dq = p.delta_h[p.q0 + q];
-                double fb = floor((sc - p.theta0[p.q0 + q]) / dq);
-                fb = fb < 0.0 ? 0.0 : (fb > double(kBins - 1) ? double(kBins - 1) : fb);
-                atomicAdd(p.hist + uint64_t(p.q0 + q) * kBins + int(fb), 1u);
-            }
-            named_bar(kAllBar, n_workers);
-            // ---- dynamic theta: raise theta_q to the lower edge of the highest bin
-            // whose suffix count of emitted survivors reaches n (a valid lower bound
-            // on the final n-th survivor score), and rewrite the query's X block.
-            bool wrote = false;
-            for (uint32_t q = uint32_t(warp); q < p.nq; q += n_worker_warps) {
-                const uint32_t* hp = p.hist + uint64_t(p.q0 + q) * kBins;
-                uint32_t sh = __ldcg(hp + 32 + lane), sl2 = __ldcg(hp + lane);
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t a = __shfl_down_sync(0xffffffffu, sh, off);
-                    const uint32_t c = __shfl_down_sync(0xffffffffu, sl2, off);
-                    if (lane + off < 32) {
-                        sh += a;
-                        sl2 += c;
+                named_bar(kEpiBar, 256);
+                if (et < p.nq) {
+                    sbase[et] = scnt[et] ? atomicAdd(p.surv_count + p.q0 + et, (unsigned long long)scnt[et]) : 0ull;
+                    scnt[et] = 0;
+                }
+                named_bar(kEpiBar, 256);
+                for (uint32_t k2 = et; k2 < nt; k2 += 256) {
+                    const uint32_t ent = touched[k2];
+                    uint32_t q;
+                    uint64_t slot;
+                    int32_t a;
+                    double sc;
+                    const bool keep = survivor(ent, q, slot, a, sc);
+                    st_key[ent] = kEmptyKey;
+                    if (!keep) continue;
+                    const unsigned long long pos = sbase[q] + atomicAdd(scnt + q, 1u);
+                    if (pos < p.surv_cap) {
+                        Result r;
+                        r.score = sc;
+                        r.id = part.ids[slot];
+                        r.acc = a;
+                        r.partition = part.ordinal;
+                        r.valid = 1;
+                        p.surv[uint64_t(p.q0 + q) * p.surv_cap + pos] = r;
                     }
+                    // every emitted survivor is a final survivor of a distinct logical thread
+                    const double dq = p.delta_h[p.q0 + q];
+                    double fb = floor((sc - p.theta0[p.q0 + q]) / dq);
+                    fb = fb < 0.0 ? 0.0 : (fb > double(kBins - 1) ? double(kBins - 1) : fb);
+                    atomicAdd(hist_s + q * kBins + int(fb), 1u);
                 }
-                const uint32_t tot_hi = __shfl_sync(0xffffffffu, sh, 0);
-                sl2 += tot_hi;
-                const unsigned mh = __ballot_sync(0xffffffffu, uint64_t(sh) >= p.n);
-                const unsigned ml = __ballot_sync(0xffffffffu, uint64_t(sl2) >= p.n);
-                int B = -1;
-                if (mh) B = 32 + (31 - __clz(mh));
-                else if (ml) B = 31 - __clz(ml);
-                if (lane == 0 && B > 0) {
-                    const double edge = p.theta0[p.q0 + q] + double(B) * p.delta_h[p.q0 + q];
-                    const double th = edge - fabs(edge) * 1e-9 - 0x1p-60;
-                    if (th > theta_s[q]) {
-                        theta_s[q] = th;
-                        const XCoef x = x_coeffs(th, cq_s[q], L, lam, p.m0, p.delta, p.mmax);
-                        xc_s[q] = x.c;
-                        xe_s[q] = x.e;
-                        xg_s[q] = x.g;
-                        write_xrow(bsm, p.n_pad, w32, q, x);
-                        wrote = true;
-                    }
-                }
+                named_bar(kEpiBar, 256);
+                for (uint32_t k2 = et; k2 < p.nq * kBins; k2 += 256)
+                    if (hist_s[k2]) atomicAdd(p.hist + uint64_t(p.q0) * kBins + k2, hist_s[k2]);
+                if (et == 0) *tcount = 0;
+                named_bar(kEpiBar, 256);
             }
-            if (wrote) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            named_bar(kAllBar, n_workers);
+#ifdef RBE_PHASE_PROF
+            const long long e2c = clock64();
+            if (p.prof && et == 32) {
+                p.prof[uint64_t(1024 + blockIdx.x) * 8 + 3] += e1c - e0c;
+                p.prof[uint64_t(1024 + blockIdx.x) * 8 + 4] += e2c - e1c;
+            }
+#endif
+            // ---- dynamic theta (one thread per query): raise theta_q to the lower edge of the
+            // highest histogram bin whose suffix count of emitted survivors reaches n (a valid
+            // lower bound on the final n-th survivor score: every emitted survivor is the final
+            // per-thread best of a distinct logical thread), then rewrite the X block of parity
+            // sidx&1, used next by strip sidx+2 (whose MMAs wait for x_ready).
+            {
+                int32_t* xw = xcoef + (sidx & 1) * 3 * kQPass;
+                uint8_t* xbw = xsm + (sidx & 1) * p.n_pad * 32;
+                bool ok16 = true;
+                if (et < p.nq) {
+                    const uint32_t q = et;
+                    const uint32_t* hp = p.hist + uint64_t(p.q0 + q) * kBins;
+                    uint64_t suffix = 0;
+                    int B = -1;
+                    for (int b0 = kBins - 16; b0 >= 0 && B < 0; b0 -= 16) {
+                        uint32_t h[16];
+#pragma unroll
+                        for (int t = 0; t < 16; ++t) h[t] = __ldcg(hp + b0 + t);
+#pragma unroll
+                        for (int t = 15; t >= 0; --t) {
+                            suffix += h[t];
+                            if (B < 0 && suffix >= p.n) B = b0 + t;
+                        }
+                    }
+                    if (B > 0) {
+                        const double edge = p.theta0[p.q0 + q] + double(B) * p.delta_h[p.q0 + q];
+                        const double th = edge - fabs(edge) * 1e-9 - 0x1p-60;
+                        if (th > theta_s[q]) theta_s[q] = th;
+                    }
+                    const XCoef x = x_coeffs(theta_s[q], cq_s[q], L, lam, p.m0, p.delta, p.mmax);
+                    xw[q] = x.c;
+                    xw[kQPass + q] = x.e;
+                    xw[2 * kQPass + q] = x.g;
+                    write_xrow(xbw, p.n_pad, 0, q, x);
+                    ok16 = p.f16max != 0 && x.c <= 32767 - p.f16max;
+                }
+                ok16 = __syncthreads_and_named(ok16);
+                if (et == 0) p16ok[sidx & 1] = ok16 ? 1u : 0u;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                named_bar(kEpiBar, 256);
+                if (et == 0) mbar_arrive(x_ready + (sidx & 1));
+#ifdef RBE_PHASE_PROF
+                if (p.prof && et == 32) p.prof[uint64_t(1024 + blockIdx.x) * 8 + 6] += clock64() - e2c;
+#endif
+            }
+#ifdef RBE_PHASE_PROF
+            RBE_CLK(c4);
+            t_end += c4 - c3;
+#endif
         }
         if (!PROBE) {
             unsigned long long sc64 = (unsigned long long)scored * p.nq, cd64 = cands;
@@ -926,10 +1139,21 @@ __global__ void __launch_bounds__(kMaxThreads, 1) tensor_scan_kernel(TensorParam
                 atomicAdd(p.candidates, cd64);
             }
         }
+#ifdef RBE_PHASE_PROF
+        if (p.prof && lane == 0 && warp == 9) {
+            unsigned long long* pr = p.prof + uint64_t(blockIdx.x) * 8;
+            pr[0] += t_wait;
+            pr[1] += t_work;
+            pr[2] += t_end;
+            pr[6] += t_ld;
+            pr[7] += t_red;
+            pr[5] += 1;
+        }
+#endif
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == producer_warp) {
+    if (warp == kProducerWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
     }
@@ -1079,7 +1303,7 @@ template <int KP, bool RW, bool PROBE>
 void launch_kernel(const TensorParams& tp, size_t smem, int grid, cudaStream_t st) {
     auto k = tensor_scan_kernel<KP, RW, PROBE>;
     RBE_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k<<<grid, 32 * (5 * tp.nwg + 1), smem, st>>>(tp);
+    k<<<grid, kThreads, smem, st>>>(tp);
     RBE_CK(cudaGetLastError());
 }
 
@@ -1106,10 +1330,10 @@ void dispatch(uint32_t kp, bool rw, const TensorParams& tp, size_t smem, int gri
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-// worker warpgroups: as many as the TMEM budget (512 columns) allows
-uint32_t pick_nwg(uint32_t w32) {
-    for (uint32_t nwg = kMaxWG; nwg >= 2; --nwg)
-        if (nwg * (2 * 8 * (w32 + 1) + kQPass) <= 512) return nwg;
+// TMEM: kSlots A operands (K = 32 (w32 + 1) bytes) and kSlots accumulators of 64 columns
+uint32_t pick_slots(uint32_t w32) {
+    for (uint32_t n = kSlots; n >= 2; n -= 2)
+        if (n * (8 * (w32 + 1) + kQPass) <= 512) return n;
     return 0;
 }
 
@@ -1122,14 +1346,19 @@ uint32_t pick_stages(uint32_t kp, uint32_t w32, uint32_t sw) {
 
 // lambda = 2^shift: the largest with |2 lambda rq| <= 127 and the data part of
 // F strictly inside the range the X block can offset (all-pass / none-pass).
+// Prefers the largest lambda whose data part leaves room for c_q within int16 (the packed
+// 16-bit epilogue, sigma K rqmax vmax <= 28000), else the largest that fits the X block.
 int pick_lam_shift(const Shape& s, uint32_t qp) {
     const uint64_t rqmax = s.rw ? ((1ull << qp) - 1) : qp;
     const uint64_t vmax = s.rw ? ((1ull << s.kp) - 1) : s.kp;
     const uint64_t K = 32ull * s.w32;
-    for (int sh = 6; sh >= 0; --sh) {
-        const uint64_t sigma = 2ull << sh;
-        if (sigma * rqmax <= 127 && sigma * rqmax * vmax * K < uint64_t(kXMax)) return sh;
-    }
+    for (int pass = 0; pass < 2; ++pass)
+        for (int sh = 6; sh >= 0; --sh) {
+            const uint64_t sigma = 2ull << sh;
+            if (sigma * rqmax > 127 || sigma * rqmax * vmax * K >= uint64_t(kXMax)) continue;
+            if (pass == 0 && sigma * rqmax * vmax * K > 28000) continue;
+            return sh;
+        }
     return -1;
 }
 
@@ -1162,10 +1391,14 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
     if (s.rw ? qp > 6 : qp > 63) return no("query planes exceed the s8 operand range");
     if (s.wpp > 4) return no("dim > 256");
     if (Q == 0) return no("no queries");
-    if (pick_nwg(s.w32) == 0) return no("tensor memory");
+    if (!pick_slots(s.w32)) return no("tensor memory");
     if (pick_stages(s.kp, s.w32, strip_width(g)) == 0) return no("shared memory");
     if (pick_lam_shift(s, qp) < 0) return no("accumulator range exceeds the threshold block");
-    if (g.items_per_thread >= (1u << 26)) return no("items_per_thread >= 2^26");
+    if (g.items_per_thread >= 511) return no("items_per_thread >= 511 (state key)");
+    {
+        const uint64_t rqmax = s.rw ? ((1ull << qp) - 1) : qp, vmax = s.rw ? ((1ull << s.kp) - 1) : s.kp;
+        if (64ull * s.wpp * rqmax * vmax >= (1ull << 22)) return no("accumulator range exceeds the state key");
+    }
     return true;
 }
 
@@ -1236,9 +1469,16 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.tpb = a.tpb;
     tp.ipt = a.ipt;
     tp.w32 = s.w32;
-    tp.nwg = pick_nwg(s.w32);
-    if (const char* e = getenv("RBE_NWG")) tp.nwg = std::min<uint32_t>(tp.nwg, uint32_t(atoi(e)));
     tp.sw = strip_width(g_of(a));
+    tp.nslots = pick_slots(s.w32);
+    if (const char* e = getenv("RBE_DBG")) tp.dbg = uint32_t(atoi(e));
+    {
+        // D_sigma <= sigma * vmax * K * rqmax; the packed epilogue is used per strip when every live
+        // query's c_q keeps that bound + c_q within int16
+        const uint64_t rqmax = s.rw ? ((1ull << a.qp) - 1) : a.qp, vmax = s.rw ? ((1ull << s.kp) - 1) : s.kp;
+        const uint64_t dmax = (2ull << lam_shift) * vmax * (64ull * s.wpp) * rqmax;
+        tp.f16max = dmax < 32767 ? int32_t(dmax) : 0;
+    }
     tp.nstages = pick_stages(s.kp, s.w32, tp.sw);
     tp.ptop = plan.ptop;
     tp.n_pad = n_pad;
@@ -1267,19 +1507,14 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     const int grid = int(std::min<uint64_t>(n_strips, uint64_t(sm_count())));
     static unsigned long long* d_prof = nullptr;
     const bool prof = getenv("RBE_PROF") != nullptr;
-    if (prof && !d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 1024 * kMaxWG * 8));
+    if (prof && !d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 2048 * 8));
     for (uint32_t ps = 0; ps < passes; ++ps) {
         tp.q0 = ps * kQPass;
         tp.nq = std::min<uint32_t>(kQPass, Q - tp.q0);
         tp.bimg = bimg + size_t(ps) * pass_bytes;
         // probe pass -> theta
         tp.probe_tiles = plan.probe_tiles;
-        {
-            // probe: each warpgroup's lanes must always hold the same logical threads
-            TensorParams pp = tp;
-            if (tp.sw > 128) pp.nwg = tp.sw / 128;
-            dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
-        }
+        dispatch<true>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
         const size_t tsm = size_t(kThetaCap) * 4;
         RBE_CK(cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsm)));
         theta_kernel<<<tp.nq, 1024, tsm, st>>>(probe + uint64_t(tp.q0) * per_query, per_query, plan.n, tp.L,
@@ -1288,23 +1523,31 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
         // main pass
         tp.probe_tiles = 0;
         if (prof) {
-            RBE_CK(cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * grid * kMaxWG * 8, st));
+            RBE_CK(cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * 2048 * 8, st));
             tp.prof = d_prof;
         }
         dispatch<false>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, false).total, grid, st);
         tp.prof = nullptr;
         if (prof) {
-            std::vector<unsigned long long> h(size_t(grid) * kMaxWG * 8);
+            std::vector<unsigned long long> h(size_t(2048) * 8);
             RBE_CK(cudaMemcpyAsync(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost, st));
             RBE_CK(cudaStreamSynchronize(st));
+            {
+                double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int b = 0; b < grid; ++b)
+                    for (int k = 0; k < 8; ++k) m[k] += double(h[size_t(1024 + b) * 8 + k]);
+                fprintf(stderr, "[rbe prof] MMA warp 0 per sub-tile: waiting for A %.0f, for D free %.0f, issuing %.0f cycles\n",
+                        m[0] / m[5], m[1] / m[5], m[2] / m[5]);
+                fprintf(stderr, "[rbe prof] strip ends per CTA: candidates %.0f, emission %.0f, theta refresh %.0f cycles\n",
+                        m[3] / grid, m[4] / grid, m[6] / grid);
+            }
             double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int b = 0; b < grid; ++b)
-                for (int w = 0; w < kMaxWG; ++w)
-                    for (int k = 0; k < 8; ++k) acc[k] += double(h[(size_t(b) * kMaxWG + w) * 8 + k]);
-            fprintf(stderr, "[rbe prof] producer: waiting for free slots %.1f%% of its time\n", 100.0 * acc[6] / acc[7]);
-            fprintf(stderr, "[rbe prof] per WG sub-tile cycles: wait_full %.0f expand %.0f wait_mma %.0f epilogue %.0f "
-                            "bar+issue %.0f (n=%.0f)\n",
-                    acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[4] / acc[5], acc[5]);
+                for (int k = 0; k < 8; ++k) acc[k] += double(h[size_t(b) * 8 + k]);
+            fprintf(stderr, "[rbe prof] per CTA: epilogue warp waiting for D %.0f cycles, testing %.0f, strip ends %.0f; "
+                            "expand warp waiting %.0f, expanding %.0f; epilogue: ld %.0f, ld+reduce %.0f\n",
+                    acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[4] / acc[5],
+                    acc[6] / acc[5], acc[7] / acc[5]);
         }
         launches += 3;
     }
