@@ -62,13 +62,12 @@ namespace rbe_dev {
 namespace {
 
 constexpr int kStages = 12;          // max ring depth (stages of sw docs)
-constexpr int kThreads = 640;        // 20 warps (roles: see tensor_scan_kernel), 96 registers each
-constexpr int kProducerWarp = 16;
-constexpr int kMmaWarp0 = 17;
-constexpr int kMmaWarps = 2;         // MMA issuer warps 17..19 (issue latency, not the tensor pipe, bounds one issuer)
-constexpr int kSlots = 4;            // A and D slots in TMEM (sub-tiles in flight)
+constexpr int kMaxWG = 3;            // worker warpgroups
+constexpr int kThreads = 512;        // 16 warps (roles: see tensor_scan_kernel), 128 registers each
+constexpr int kProducerWarp = 12;
+constexpr int kMmaWarp0 = 13;        // one MMA issuer warp per worker warpgroup
 constexpr uint32_t kCandQueue = 4096;  // deferred candidates per strip (shared memory; overflow is scored at once)
-constexpr int kEpiBar = 8;           // named barrier of the 256 epilogue threads
+constexpr int kAllBar = 8;           // named barrier of all worker threads
 constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
 constexpr uint32_t kEmptyKey = ~0u;      // state key: (i << 23) | (acc & 0x7fffff), i < 511, |acc| < 2^22
 constexpr int kBins = 64;            // dynamic-theta histogram bins per query
@@ -83,7 +82,7 @@ struct TensorParams {
     uint32_t tpb, ipt;
     uint32_t w32;                  // u32 words per doc plane (= data K blocks)
     uint32_t nstages;              // ring depth (stages of sw docs)
-    uint32_t nslots;               // A / D slots in TMEM (2 or kSlots)
+    uint32_t nwg;                  // worker warpgroups (2 or 3)
     uint32_t dbg;                  // debugging/timing experiments (RBE_DBG): 1 = epilogue skips TMEM loads,
                                    // 2 = expand skips TMEM stores (results invalid)
     int32_t f16max;                // F <= f16max - c_q for every pair: the low 16 bits keep the sign of any
@@ -177,13 +176,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-// AND of a predicate over the 256 epilogue threads (named barrier 8 with .red.and)
-__device__ __forceinline__ bool __syncthreads_and_named(bool pred) {
+// AND of a predicate over the n worker threads (named barrier kAllBar with .red.and)
+__device__ __forceinline__ bool bar_and(bool pred, uint32_t n) {
     uint32_t r;
     asm volatile(
-        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, 8, 256, p;\n\tselp.u32 %0, 1, 0, q;\n}"
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.and.pred q, 8, %2, p;\n\tselp.u32 %0, 1, 0, q;\n}"
         : "=r"(r)
-        : "r"(uint32_t(pred))
+        : "r"(uint32_t(pred)), "r"(n)
         : "memory");
     return r != 0;
 }
@@ -440,7 +439,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uin
     s.qconst = off;
     off = al(off + kQPass * 8 + kQPass * 4 + 2 * 3 * kQPass * 4 + 16);
     s.bars = off;
-    off = al(off + (2 * nstages + 4 * kSlots + 4) * 8 + 32);
+    off = al(off + (2 * nstages + 2 * kMaxWG + 2) * 8 + 32);
     s.total = off;
     return s;
 }
@@ -476,26 +475,24 @@ __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, ui
     }
 }
 
-// phase timing of the epilogue loop (build with -DRBE_PHASE_PROF and run with RBE_PROF=1)
-#ifdef RBE_PHASE_PROF
-#define RBE_CLK(x) const long long x = clock64()
-#else
-#define RBE_CLK(x)
-#endif
-
-// Warp roles (20 warps, 96 registers each):
-//   warps 0-7    expand: group e = warp/4 takes sub-tiles u = e (mod 2); quadrant warp%4
-//   warps 8-15   epilogue: group e = (warp-8)/4 takes sub-tiles u = e (mod 2)
-//   warp 16      producer (ring of stages; TMEM allocator)
-//   warps 17-19  MMA issuers: warp 17+m takes sub-tiles u = m (mod 3)
-// Sub-tile u (128 docs, CTA-local counter) uses A slot u % kSlots and D slot u % kSlots.
+// Warp roles (16 warps, 128 registers each):
+//   warps 0..4*nwg-1   workers: warpgroup w = warp/4 takes sub-tiles u = w (mod nwg)
+//                      (128 docs, CTA-local counter u); quadrant warp%4 = TMEM lanes.
+//                      Per warpgroup, software-pipelined within a strip:
+//                        expand(k+1) -> A[(k+1)&1] while the tensor core runs MMA(k);
+//                        wait MMA(k); test D; arrive a_full (A(k+1) ready, D free)
+//   warp 12            producer: one contiguous sw-doc stage per tile; TMEM allocator
+//   warps 13..13+nwg-1 MMA issuers, one per warpgroup (whole warp, elected lane)
 template <int KP, bool RW, bool PROBE>
 __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t w32 = p.w32;
     const uint32_t nst = p.nstages;
+    const uint32_t nwg = p.nwg;                              // 2 or 3
+    const uint32_t n_workers = 128 * nwg;
     const uint32_t sw = p.sw;                                // strip width (logical threads): 128 or 256
     const uint32_t spt = sw / 128;                           // 128-doc sub-tiles per stage
+    const uint32_t spt_sh = spt == 2 ? 1 : 0;
     const uint32_t plane_bytes = sw * w32 * 4;               // one plane of a stage (sw docs)
     const uint32_t stage_bytes = KP * plane_bytes + sw * 4;  // + the stage's f32 magnitudes
     SmemLayout sl = smem_layout(KP, w32, p.n_pad, nst, sw, PROBE);
@@ -503,35 +500,30 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     uint8_t* bsm = smem + sl.b;
     uint8_t* xsm = smem + sl.xb;  // [2][n_pad * 32]
     uint32_t* st_key = reinterpret_cast<uint32_t*>(smem + sl.state);  // [64][sw]
-    float* pmax = reinterpret_cast<float*>(smem + sl.state);                              // probe: [64][sw]
-    uint2* cqueue = reinterpret_cast<uint2*>(smem + sl.cqueue);     // deferred candidates
-    double* theta_s = reinterpret_cast<double*>(smem + sl.qconst);  // [64]
-    int32_t* cq_s = reinterpret_cast<int32_t*>(theta_s + kQPass);   // [64]
-    int32_t* xcoef = cq_s + kQPass;                                 // [2][3][64]: c, e, g per strip parity
+    float* pmax = reinterpret_cast<float*>(smem + sl.state);          // probe: [64][sw]
+    uint2* cqueue = reinterpret_cast<uint2*>(smem + sl.cqueue);       // deferred candidates
+    uint16_t* touched = reinterpret_cast<uint16_t*>(smem + sl.touched);  // state entries set in the strip
+    double* theta_s = reinterpret_cast<double*>(smem + sl.qconst);    // [64]
+    int32_t* cq_s = reinterpret_cast<int32_t*>(theta_s + kQPass);     // [64]
+    int32_t* xcoef = cq_s + kQPass;                                   // [2][3][64]: c, e, g per strip parity
     uint32_t* p16ok = reinterpret_cast<uint32_t*>(xcoef + 2 * 3 * kQPass);  // [2] packed epilogue safe
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sl.bars);
-    uint64_t* full = bars;                  // [nst]    stage loaded (tx bytes)
-    uint64_t* empty = full + nst;           // [nst]    stage consumed (4 warp arrivals per sub-tile)
-    uint64_t* a_full = empty + nst;         // [kSlots] A written (4 expand warps)
-    uint64_t* a_free = a_full + kSlots;     // [kSlots] MMA done reading A (commit)
-    uint64_t* d_full = a_free + kSlots;     // [kSlots] D ready (commit)
-    uint64_t* d_free = d_full + kSlots;     // [kSlots] D read (4 epilogue warps)
-    uint64_t* x_ready = d_free + kSlots;    // [2]      X block of parity b rewritten (refresher)
-    uint64_t* emitted = x_ready + 2;        // [2]      strip of parity b emitted (epilogue)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(emitted + 2);
+    uint64_t* full = bars;                // [nst]   stage loaded (tx bytes)
+    uint64_t* empty = full + nst;         // [nst]   stage consumed (4 warp arrivals per sub-tile)
+    uint64_t* a_full = empty + nst;       // [kMaxWG] A complete and D free (4 warp arrivals)
+    uint64_t* mma_done = a_full + kMaxWG; // [kMaxWG] MMA committed
+    uint64_t* x_ready = mma_done + kMaxWG;  // [2] X block of parity b rewritten (strip end)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_ready + 2);
     uint32_t* cq_count = tmem_slot + 1;
     uint32_t* tcount = tmem_slot + 2;
-    uint16_t* touched = reinterpret_cast<uint16_t*>(smem + sl.touched);  // [64 * sw] state entries set in the strip
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t a_cols = 8 * (w32 + 1);  // TMEM columns of one A (4 K bytes per column)
     const uint32_t d_cols = p.n_pad;        // TMEM columns of one D
+    const uint32_t wg_cols = 2 * a_cols + d_cols;
     uint32_t tmem_cols = 32;
-    const uint32_t nsl = p.nslots;                  // 2 or 4
-    const uint32_t nsl_sh = nsl == 4 ? 2 : 1;
-    const uint32_t spt_sh = spt == 2 ? 1 : 0;
-    while (tmem_cols < nsl * (a_cols + d_cols)) tmem_cols <<= 1;
+    while (tmem_cols < nwg * wg_cols) tmem_cols <<= 1;
     const int L = int(p.L);
     const double lam = double(1u << p.lam_shift);
 
@@ -565,16 +557,12 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             mbar_init(full + s, 1);
             mbar_init(empty + s, 4 * spt);
         }
-        for (int k = 0; k < kSlots; ++k) {
-            mbar_init(a_full + k, 4);
-            mbar_init(a_free + k, 1);
-            mbar_init(d_full + k, 1);
-            mbar_init(d_free + k, 4);
+        for (int w = 0; w < kMaxWG; ++w) {
+            mbar_init(a_full + w, 4);
+            mbar_init(mma_done + w, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(x_ready + b, 1);
-            mbar_init(emitted + b, 1);
-        }
+        mbar_init(x_ready + 0, 1);
+        mbar_init(x_ready + 1, 1);
         *cq_count = 0;
         *tcount = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -590,8 +578,6 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    auto a_addr = [&](uint32_t slot) { return tmem_base + slot * a_cols; };
-    auto d_addr = [&](uint32_t slot) { return tmem_base + nsl * a_cols + slot * d_cols; };
 
     if (warp == kProducerWarp) {
         // ===================== producer: one contiguous sw-doc stage per tile of each strip =====================
@@ -613,292 +599,215 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 }
             }
         }
-    } else if (warp >= kMmaWarp0 && warp < kMmaWarp0 + kMmaWarps) {
-        // ===================== MMA issuers: sub-tiles u = m (mod 2) in order =====================
-        const uint32_t m = uint32_t(warp - kMmaWarp0);
-        {
-            // the whole warp runs this loop (operands stay warp-uniform); one lane issues
-            const uint32_t idesc = idesc_i8(128, p.n_pad);
-            const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
-            const uint64_t x_desc0 = smem_desc(smem_u32(xsm));
-            const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
-            uint32_t u0 = 0, sidx = 0;
-            for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
-                const StripInfo si = strip_info(p, s);
-                const uint32_t n_sub = si.n_tiles * spt;
-                if (!PROBE && sidx >= 2 && n_sub > 0) {
-                    // X block of parity sidx&1 was rewritten at the end of strip sidx-2
-                    mbar_wait_sleep(x_ready + (sidx & 1), ((sidx - 2) >> 1) & 1);
-                }
-                const uint64_t xd = x_desc0 + (sidx & 1) * b_step;
-                // warp m issues the sub-tiles of slots = m (mod kMmaWarps): each of its
-                // barriers is visited at every use, so parity waits are unambiguous
-                for (uint32_t k = (m + kMmaWarps - u0 % kMmaWarps) % kMmaWarps; k < n_sub; k += kMmaWarps) {
-                    const uint32_t u = u0 + k, slot = u & (nsl - 1), use = u >> nsl_sh;
-#ifdef RBE_PHASE_PROF
-                    const long long m0c = clock64();
-#endif
-                    mbar_wait_sleep(a_full + slot, use & 1);
-#ifdef RBE_PHASE_PROF
-                    const long long m1c = clock64();
-#endif
-                    mbar_wait_sleep(d_free + slot, (use & 1) ^ 1);
-#ifdef RBE_PHASE_PROF
-                    const long long m2c = clock64();
-                    if (p.prof && m == 0 && lane == 0) {
-                        p.prof[uint64_t(1024 + blockIdx.x) * 8 + 0] += m1c - m0c;
-                        p.prof[uint64_t(1024 + blockIdx.x) * 8 + 1] += m2c - m1c;
-                        p.prof[uint64_t(1024 + blockIdx.x) * 8 + 5] += 1;
-                    }
-#endif
-                    tc_fence_after();
-                    const uint32_t a_t = a_addr(slot), d_t = d_addr(slot);
-                    switch (w32) {
-                        case 2: mma_group<2>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                        case 4: mma_group<4>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                        case 6: mma_group<6>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                        default: mma_group<8>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                    }
-                    mma_commit_elect(d_full + slot);  // D ready and A free (expand waits on it too)
-                    __syncwarp();
-#ifdef RBE_PHASE_PROF
-                    if (p.prof && m == 0 && lane == 0) p.prof[uint64_t(1024 + blockIdx.x) * 8 + 2] += clock64() - m2c;
-#endif
-                }
-                u0 += n_sub;
-            }
-        }
-    } else if (warp < 8) {
-        // ===================== expand warps =====================
-        const uint32_t e = uint32_t(warp >> 2);
-        const int quad = warp & 3;
-        const uint32_t l = uint32_t(quad * 32 + lane);
-        const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        {
-            // constant columns 2..7 of the X block of every A slot (K bytes 8..31 = 255)
-            uint32_t v[8] = {0u, 0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u};
-            for (uint32_t k = e; k < nsl; k += 2) tmem_st8(a_addr(k) + lane_base + 8 * w32, v);
-            tmem_wait_st();
-        }
-#ifdef RBE_PHASE_PROF
-        long long x_wait = 0, x_work = 0;
-#endif
-        uint32_t u0 = 0, tiles0 = 0;
-        for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
+    } else if (warp >= kMmaWarp0 && warp < kMmaWarp0 + int(nwg)) {
+        // ===================== MMA issuer of warpgroup w (whole warp, one elected lane issues) =====================
+        const uint32_t w = uint32_t(warp - kMmaWarp0);
+        const uint32_t idesc = idesc_i8(128, p.n_pad);
+        const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
+        const uint64_t x_desc0 = smem_desc(smem_u32(xsm));
+        const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
+        const uint32_t a_base = tmem_base + w * wg_cols;
+        const uint32_t d_t = a_base + 2 * a_cols;
+        uint32_t c = 0, u0 = 0, sidx = 0;
+        for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
             const StripInfo si = strip_info(p, s);
             const uint32_t n_sub = si.n_tiles * spt;
-            uint32_t k = (e + 2 - (u0 & 1)) & 1;
-            if (k < n_sub) {
-                uint32_t ti = k / spt;
-                uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
-                for (; k < n_sub; k += 2) {
-                    for (const uint32_t tn = k >> spt_sh; ti < tn; ++ti)
-                        if (++st_idx == nst) {
-                            st_idx = 0;
-                            st_ph ^= 1;
-                        }
-                    const uint32_t u = u0 + k, slot = u & (nsl - 1), use = u >> nsl_sh;
-                    const uint32_t col = (k & (spt - 1)) * 128 + l;
-#ifdef RBE_PHASE_PROF
-                    const long long tw0 = clock64();
-#endif
-                    mbar_wait_sleep(full + st_idx, st_ph);
-                    mbar_wait_sleep(d_full + slot, (use & 1) ^ 1);  // MMA(u - nsl) done: A slot free
-#ifdef RBE_PHASE_PROF
-                    const long long tw1 = clock64();
-                    x_wait += tw1 - tw0;
-#endif
-                    tc_fence_after();
-                    const uint8_t* stage = ring + st_idx * stage_bytes;
-                    const uint32_t a_t = a_addr(slot) + lane_base;
-                    if ((w32 & 3) == 0) {
-                        // 16-byte loads: a warp reads 32 consecutive docs x 16 B = 512 B, conflict-free
-                        const uint4* src = reinterpret_cast<const uint4*>(stage);
-                        const uint32_t w128 = w32 / 4;
-                        for (uint32_t g4 = 0; g4 < w128; ++g4) {
-                            uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
-#pragma unroll
-                            for (int t = 0; t < KP; ++t) {
-                                const uint4 v = src[(t * sw + col) * w128 + g4];
-                                w0[t] = v.x;
-                                w1[t] = v.y;
-                                w2[t] = v.z;
-                                w3[t] = v.w;
-                            }
-                            uint32_t out[16];
-                            Expand<KP, RW>::run(w0, out);
-                            Expand<KP, RW>::run(w1, out + 8);
-                            if (p.dbg & 2) {
-                                if (out[0] == 0x12345678u) tmem_st16(a_t + 32 * g4, out);
-                            } else {
-                                tmem_st16(a_t + 32 * g4, out);
-                            }
-                            Expand<KP, RW>::run(w2, out);
-                            Expand<KP, RW>::run(w3, out + 8);
-                            if (p.dbg & 2) {
-                                if (out[0] == 0x12345678u) tmem_st16(a_t + 32 * g4 + 16, out);
-                            } else {
-                                tmem_st16(a_t + 32 * g4 + 16, out);
-                            }
-                        }
-                    } else {
-                        const uint2* src = reinterpret_cast<const uint2*>(stage);
-                        const uint32_t w64 = w32 / 2;
-                        for (uint32_t g2 = 0; g2 < w64; ++g2) {
-                            uint32_t w0[KP], w1[KP];
-#pragma unroll
-                            for (int t = 0; t < KP; ++t) {
-                                const uint2 v = src[(t * sw + col) * w64 + g2];
-                                w0[t] = v.x;
-                                w1[t] = v.y;
-                            }
-                            uint32_t out[16];
-                            Expand<KP, RW>::run(w0, out);
-                            Expand<KP, RW>::run(w1, out + 8);
-                            tmem_st16(a_t + 16 * g2, out);
-                        }
-                    }
-                    const float mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
-                    const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
-                    tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
-                    tmem_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(a_full + slot);
-#ifdef RBE_PHASE_PROF
-                    x_work += clock64() - tw1;
-#endif
-                }
-            }
+            const uint32_t first = (w + nwg - u0 % nwg) % nwg;
+            const uint32_t mine = n_sub > first ? (n_sub - first + nwg - 1) / nwg : 0;
             u0 += n_sub;
-            tiles0 += si.n_tiles;
+            if (!PROBE && sidx >= 2 && mine > 0) {
+                // X block of parity sidx&1 was rewritten at the end of strip sidx-2
+                mbar_wait_sleep(x_ready + (sidx & 1), ((sidx - 2) >> 1) & 1);
+            }
+            const uint64_t xd = x_desc0 + (sidx & 1) * b_step;
+            for (uint32_t k = 0; k < mine; ++k, ++c) {
+                mbar_wait_sleep(a_full + w, c & 1);
+                tc_fence_after();
+                const uint32_t a_t = a_base + (c & 1) * a_cols;
+                switch (w32) {
+                    case 2: mma_group<2>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                    case 4: mma_group<4>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                    case 6: mma_group<6>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                    default: mma_group<8>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
+                }
+                mma_commit_elect(mma_done + w);
+                __syncwarp();
+            }
         }
-#ifdef RBE_PHASE_PROF
-        if (p.prof && lane == 0 && warp == 1) {
-            p.prof[uint64_t(blockIdx.x) * 8 + 3] += x_wait;
-            p.prof[uint64_t(blockIdx.x) * 8 + 4] += x_work;
-        }
-#endif
-    } else if (warp < 16) {
-        // ===================== epilogue warps =====================
-        const uint32_t e = uint32_t((warp - 8) >> 2);
+    } else if (warp < int(4 * nwg)) {
+        // ===================== workers =====================
+        const uint32_t wg = uint32_t(warp >> 2);
         const int quad = warp & 3;
-        const uint32_t l = uint32_t(quad * 32 + lane);
+        const uint32_t l = uint32_t(quad * 32 + lane);  // TMEM lane == doc within the sub-tile
+        const uint32_t wt = uint32_t(threadIdx.x);      // worker thread id
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        const uint32_t et = uint32_t(threadIdx.x - 256);  // epilogue thread id [0, 256)
+        const uint32_t a_t0 = tmem_base + wg * wg_cols + lane_base;  // this warpgroup's A[0] (this warp's lanes)
+        const uint32_t d_t = tmem_base + wg * wg_cols + 2 * a_cols + lane_base;
         const uint32_t pstride = p.ptop;
         uint32_t scored = 0, cands = 0;
+        uint32_t kc = 0;  // sub-tiles processed by this warpgroup (A buffer / barrier parities)
         float pm[PROBE ? kQPass : 1];
 #pragma unroll
-        for (int k2 = 0; k2 < (PROBE ? kQPass : 1); ++k2) pm[k2] = -INFINITY;
-#ifdef RBE_PHASE_PROF
-        long long t_wait = 0, t_work = 0, t_end = 0, t_ld = 0, t_red = 0;
-#endif
+        for (int e = 0; e < (PROBE ? kQPass : 1); ++e) pm[e] = -INFINITY;
+        {
+            // constant columns 2..7 of the X block of both A buffers (K bytes 8..31 = 255)
+            uint32_t v[8] = {0u, 0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u};
+            tmem_st8(a_t0 + 8 * w32, v);
+            tmem_st8(a_t0 + a_cols + 8 * w32, v);
+            tmem_wait_st();
+        }
+
+        // expand doc `col` of ring stage `st` into A buffer `ab`; returns its magnitude and bin
+        auto expand = [&](uint32_t st, uint32_t col, uint32_t ab, float& mag, uint32_t& j) {
+            const uint8_t* stage = ring + st * stage_bytes;
+            const uint32_t a_t = a_t0 + ab * a_cols;
+            if ((w32 & 3) == 0) {
+                // 16-byte loads: a warp reads 32 consecutive docs x 16 B = 512 B, conflict-free
+                const uint4* src = reinterpret_cast<const uint4*>(stage);
+                const uint32_t w128 = w32 / 4;
+                for (uint32_t g4 = 0; g4 < w128; ++g4) {
+                    uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
+#pragma unroll
+                    for (int t = 0; t < KP; ++t) {
+                        const uint4 v = src[(t * sw + col) * w128 + g4];
+                        w0[t] = v.x;
+                        w1[t] = v.y;
+                        w2[t] = v.z;
+                        w3[t] = v.w;
+                    }
+                    uint32_t out[16];
+                    Expand<KP, RW>::run(w0, out);
+                    Expand<KP, RW>::run(w1, out + 8);
+                    tmem_st16(a_t + 32 * g4, out);
+                    Expand<KP, RW>::run(w2, out);
+                    Expand<KP, RW>::run(w3, out + 8);
+                    tmem_st16(a_t + 32 * g4 + 16, out);
+                }
+            } else {
+                const uint2* src = reinterpret_cast<const uint2*>(stage);
+                const uint32_t w64 = w32 / 2;
+                for (uint32_t g2 = 0; g2 < w64; ++g2) {
+                    uint32_t w0[KP], w1[KP];
+#pragma unroll
+                    for (int t = 0; t < KP; ++t) {
+                        const uint2 v = src[(t * sw + col) * w64 + g2];
+                        w0[t] = v.x;
+                        w1[t] = v.y;
+                    }
+                    uint32_t out[16];
+                    Expand<KP, RW>::run(w0, out);
+                    Expand<KP, RW>::run(w1, out + 8);
+                    tmem_st16(a_t + 16 * g2, out);
+                }
+            }
+            mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
+            j = mag_bin(mag, p.m0f, p.inv_df);
+            tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + st);  // this warp's share of the stage is consumed
+        };
+        // this warp's part of A is complete and its D reads are done: one arrival per warp
+        auto arrive_a = [&]() {
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full + wg);
+        };
+
         uint32_t u0 = 0, tiles0 = 0, sidx = 0;
         for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
             const StripInfo si = strip_info(p, s);
             const PartDesc& part = p.parts[si.part];
             const uint32_t n_sub = si.n_tiles * spt;
             const uint64_t lim = part.count > si.base ? part.count - si.base : 0;  // valid: i*tpb + col < lim
-            if (!PROBE && sidx >= 2 && n_sub > 0) mbar_wait_sleep(x_ready + (sidx & 1), ((sidx - 2) >> 1) & 1);
             const int32_t* xc = xcoef + (sidx & 1) * 3 * kQPass;
             const bool p16 = p16ok[sidx & 1] != 0;
-            uint32_t k = (e + 2 - (u0 & 1)) & 1;
-            uint32_t ti = k >> spt_sh;
-            uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
-            for (; k < n_sub; k += 2) {
-                for (const uint32_t tn = k >> spt_sh; ti < tn; ++ti)
-                    if (++st_idx == nst) {
-                        st_idx = 0;
-                        st_ph ^= 1;
-                    }
-                const uint32_t u = u0 + k, slot = u & (nsl - 1), use = u >> nsl_sh;
-                const uint32_t i = k >> spt_sh, col = (k & (spt - 1)) * 128 + l;
-                const bool valid = uint64_t(i) * p.tpb + col < lim;
-                const float* stage_mags = reinterpret_cast<const float*>(ring + st_idx * stage_bytes + KP * plane_bytes);
-                scored += valid ? 1 : 0;
-                RBE_CLK(c0);
-                mbar_wait_sleep(d_full + slot, use & 1);
-                tc_fence_after();
-                RBE_CLK(c1);
-                const uint32_t d_t = d_addr(slot) + lane_base;
-                if (PROBE) {
-                    // F = lambda acc; per-thread maxima of the (float) score
-                    mbar_wait(full + st_idx, st_ph);  // complete: the stage is held until our arrival
-                    const float mag = stage_mags[col];
-                    const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
-#pragma unroll
-                    for (int c = 0; c < kQPass / 16; ++c) {
-                        int32_t F[16];
-                        tmem_ld16(d_t + 16 * c, F);
-                        tmem_wait_ld();
-                        if (valid) {
-#pragma unroll
-                            for (int e2 = 0; e2 < 16; ++e2)
-                                pm[16 * c + e2] = fmaxf(pm[16 * c + e2], float(F[e2]) * scale);
+            uint32_t k = (wg + nwg - u0 % nwg) % nwg;
+            if (k < n_sub) {
+                uint32_t ti = k >> spt_sh;
+                uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
+                auto seek = [&](uint32_t t_new) {
+                    for (; ti < t_new; ++ti)
+                        if (++st_idx == nst) {
+                            st_idx = 0;
+                            st_ph ^= 1;
                         }
+                };
+                float mag, mag_n = 0.0f;
+                uint32_t j, j_n = 0;
+                uint32_t col = (k & (spt - 1)) * 128 + l, col_n = 0;
+                mbar_wait(full + st_idx, st_ph);
+                expand(st_idx, col, kc & 1, mag, j);
+                arrive_a();
+                while (true) {
+                    const uint32_t k_n = k + nwg;
+                    const bool has_next = k_n < n_sub;
+                    const uint32_t i = k >> spt_sh;
+                    if (has_next) {
+                        seek(k_n >> spt_sh);
+                        col_n = (k_n & (spt - 1)) * 128 + l;
+                        mbar_wait(full + st_idx, st_ph);
+                        expand(st_idx, col_n, (kc + 1) & 1, mag_n, j_n);
                     }
-                } else {
-                    // F >= 0 is necessary for score >= theta: AND the sign bits per group of 8
-                    uint32_t gmask = 0;  // bit g: some F >= 0 among queries [8g, 8g+8)
-                    if (p16) {
-                        // low 16 bits of all 64 accumulators in 32 registers (pack::16b); the
-                        // sign of every F >= 0 survives, a wrapped F < 0 is rejected exactly below
-                        uint32_t R[32];
-                        if (p.dbg & 1) {
+                    const bool valid = uint64_t(i) * p.tpb + col < lim;
+                    scored += valid ? 1 : 0;
+                    mbar_wait_sleep(mma_done + wg, kc & 1);
+                    tc_fence_after();
+                    if (PROBE) {
+                        // F = lambda acc; per-thread maxima of the (float) score
+                        const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
 #pragma unroll
-                            for (int e2 = 0; e2 < 32; ++e2) R[e2] = 0x80008000u;
-                        } else {
-                            tmem_ld32_p16(d_t, R);
+                        for (int c = 0; c < kQPass / 16; ++c) {
+                            int32_t F[16];
+                            tmem_ld16(d_t + 16 * c, F);
                             tmem_wait_ld();
-                        }
-#ifdef RBE_PHASE_PROF
-                        t_ld += clock64() - c1;
-#endif
-                        uint32_t a4[4];
+                            if (valid) {
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            uint32_t a = R[8 * g];
-#pragma unroll
-                            for (int e2 = 1; e2 < 8; ++e2) a &= R[8 * g + e2];
-                            a4[g] = a;
-                        }
-                        const uint32_t all = (a4[0] & a4[1]) & (a4[2] & a4[3]);
-                        if ((~all & 0x80008000u) && valid) {
-#pragma unroll
-                            for (int g = 0; g < kQPass / 8; ++g) {
-                                const uint32_t a = (R[4 * g] & R[4 * g + 1]) & (R[4 * g + 2] & R[4 * g + 3]);
-                                gmask |= uint32_t((~a & 0x80008000u) != 0u) << g;
+                                for (int e2 = 0; e2 < 16; ++e2)
+                                    pm[16 * c + e2] = fmaxf(pm[16 * c + e2], float(F[e2]) * scale);
                             }
                         }
                     } else {
-                        int32_t F[kQPass];
-                        tmem_ld32(d_t, F);
-                        tmem_ld32(d_t + 32, F + 32);
-                        tmem_wait_ld();
-#ifdef RBE_PHASE_PROF
-                        t_ld += clock64() - c1;
-#endif
+                        // F >= 0 is necessary for score >= theta: AND the sign bits per group of 8
+                        uint32_t gmask = 0;  // bit g: some F >= 0 among queries [8g, 8g+8)
+                        if (p16) {
+                            // low 16 bits of all 64 accumulators in 32 registers (pack::16b); the
+                            // sign of every F >= 0 survives, a wrapped F < 0 is rejected exactly below
+                            uint32_t R[32];
+                            tmem_ld32_p16(d_t, R);
+                            tmem_wait_ld();
+                            uint32_t a4[4];
 #pragma unroll
-                        for (int g = 0; g < kQPass / 8; ++g) {
-                            uint32_t a = uint32_t(F[8 * g]);
+                            for (int g = 0; g < 4; ++g) {
+                                uint32_t a = R[8 * g];
 #pragma unroll
-                            for (int e2 = 1; e2 < 8; ++e2) a &= uint32_t(F[8 * g + e2]);
-                            gmask |= (~a >> 31) << g;
+                                for (int e2 = 1; e2 < 8; ++e2) a &= R[8 * g + e2];
+                                a4[g] = a;
+                            }
+                            const uint32_t all = (a4[0] & a4[1]) & (a4[2] & a4[3]);
+                            if ((~all & 0x80008000u) && valid) {
+#pragma unroll
+                                for (int g = 0; g < kQPass / 8; ++g) {
+                                    const uint32_t a = (R[4 * g] & R[4 * g + 1]) & (R[4 * g + 2] & R[4 * g + 3]);
+                                    gmask |= uint32_t((~a & 0x80008000u) != 0u) << g;
+                                }
+                            }
+                        } else {
+                            int32_t F[kQPass];
+                            tmem_ld32(d_t, F);
+                            tmem_ld32(d_t + 32, F + 32);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int g = 0; g < kQPass / 8; ++g) {
+                                uint32_t a = uint32_t(F[8 * g]);
+#pragma unroll
+                                for (int e2 = 1; e2 < 8; ++e2) a &= uint32_t(F[8 * g + e2]);
+                                gmask |= (~a >> 31) << g;
+                            }
+                            if (!valid) gmask = 0;
                         }
-                    }
-                    if (!valid) gmask = 0;
-#ifdef RBE_PHASE_PROF
-                    t_red += clock64() - c1;
-#endif
-                    // groups with a passing pair in any lane (tcgen05.ld is warp-collective)
-                    uint32_t wmask = __reduce_or_sync(0xffffffffu, gmask);
-                    if (wmask) {
-                        // rare: re-read those groups and queue each passing pair for exact FP64
-                        // scoring at the strip end
-                        mbar_wait(full + st_idx, st_ph);  // complete: the stage is held until our arrival
-                        const float mag = stage_mags[col];
-                        const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
+                        // groups with a passing pair in any lane (tcgen05.ld is warp-collective)
+                        uint32_t wmask = __reduce_or_sync(0xffffffffu, gmask);
                         while (wmask) {
                             const uint32_t g = uint32_t(__ffs(wmask) - 1);
                             wmask &= wmask - 1;
@@ -915,6 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                                 const int32_t num = v[e2] - X;
                                 if (num & ((1 << p.lam_shift) - 1)) atomicAdd(p.error, 1u);
                                 const int32_t a = (num >> p.lam_shift) + cq_s[q];
+                                // defer to the strip end (exact FP64 scoring in bulk); score now if full
                                 const uint32_t pos = atomicAdd(cq_count, 1u);
                                 if (pos < kCandQueue)
                                     cqueue[pos] = make_uint2((q << 26) | i, (col << 24) | (uint32_t(a) & 0xffffffu));
@@ -924,41 +834,38 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                             }
                         }
                     }
+                    ++kc;
+                    if (!has_next) break;
+                    arrive_a();  // A(k+nwg) ready, D read: the MMA warp may issue
+                    k = k_n;
+                    col = col_n;
+                    mag = mag_n;
+                    j = j_n;
                 }
                 tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(d_free + slot);
-                    mbar_arrive(empty + st_idx);  // this warp's share of the stage is consumed
-                }
-#ifdef RBE_PHASE_PROF
-                RBE_CLK(c2);
-                t_wait += c1 - c0;
-                t_work += c2 - c1;
-#endif
             }
             u0 += n_sub;
             tiles0 += si.n_tiles;
-            RBE_CLK(c3);
-            // ================= strip end (all 256 epilogue threads) =================
+            // ================= strip end (all worker threads) =================
             if (PROBE) {
-                // merge the two groups' per-lane maxima (each group always holds the same
-                // logical threads when spt == 2; both hold column l when spt == 1)
-                const uint32_t colp = (e % spt) * 128 + l;
-                for (uint32_t w = 0; w < 2; ++w) {
-                    if (w == e) {
+                // merge the warpgroups' per-lane maxima: the lanes of warpgroup w always hold
+                // logical threads (w % spt) * 128 + l when nwg is a multiple of spt; otherwise
+                // (spt == 2, nwg == 3) the probe runs with one column per warpgroup (host)
+                const uint32_t colp = (wg % spt) * 128 + l;
+                for (uint32_t w = 0; w < nwg; ++w) {
+                    if (w == wg) {
 #pragma unroll
-                        for (int k2 = 0; k2 < kQPass; ++k2) {
-                            float* mm = pmax + k2 * sw + colp;
-                            *mm = fmaxf(*mm, pm[k2]);
-                            pm[k2] = -INFINITY;
+                        for (int e = 0; e < kQPass; ++e) {
+                            float* m = pmax + e * sw + colp;
+                            *m = fmaxf(*m, pm[e]);
+                            pm[e] = -INFINITY;
                         }
                     }
-                    named_bar(kEpiBar, 256);
+                    named_bar(kAllBar, n_workers);
                 }
                 // per query keep the top ptop per-thread maxima of the strip (distinct threads)
                 const uint32_t vpl = sw / 32;
-                for (uint32_t q = uint32_t(warp - 8); q < p.nq; q += 8) {
+                for (uint32_t q = uint32_t(warp); q < p.nq; q += 4 * nwg) {
                     float v[8];
 #pragma unroll
                     for (int k2 = 0; k2 < 8; ++k2) v[k2] = uint32_t(k2) < vpl ? pmax[q * sw + 32 * k2 + lane] : -INFINITY;
@@ -981,19 +888,16 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         if (lane == 0) p.probe_out[(uint64_t(p.q0 + q) * p.n_strips + s) * pstride + r] = mx;
                     }
                 }
-                named_bar(kEpiBar, 256);
-                for (uint32_t k2 = et; k2 < kQPass * sw; k2 += 256) pmax[k2] = -INFINITY;
-                named_bar(kEpiBar, 256);
+                named_bar(kAllBar, n_workers);
+                for (uint32_t k2 = wt; k2 < kQPass * sw; k2 += n_workers) pmax[k2] = -INFINITY;
+                named_bar(kAllBar, n_workers);
                 continue;
             }
-            named_bar(kEpiBar, 256);
-#ifdef RBE_PHASE_PROF
-            const long long e0c = clock64();
-#endif
+            named_bar(kAllBar, n_workers);
             // exact FP64 scoring of the strip's deferred candidates
             {
                 const uint32_t nc = min(*cq_count, uint32_t(kCandQueue));
-                for (uint32_t k2 = et; k2 < nc; k2 += 256) {
+                for (uint32_t k2 = wt; k2 < nc; k2 += n_workers) {
                     const uint2 c = cqueue[k2];
                     const uint32_t q = c.x >> 26, ii = c.x & 0x3ffffffu, cc = c.y >> 24;
                     const int32_t a = int32_t(c.y << 8) >> 8;
@@ -1002,22 +906,19 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                                    tcount);
                 }
             }
-            named_bar(kEpiBar, 256);
-            if (et == 0) *cq_count = 0;
-#ifdef RBE_PHASE_PROF
-            const long long e1c = clock64();
-#endif
+            named_bar(kAllBar, n_workers);
+            if (wt == 0) *cq_count = 0;
             // emit the strip's survivors >= theta (one per (query, logical thread)) from the
             // list of state entries set in this strip: pass 1 counts per query, one global
             // reservation per query, pass 2 writes; the histogram is merged in shared memory
             {
-                uint32_t* scnt = reinterpret_cast<uint32_t*>(cqueue);       // [64] per-query counters
+                uint32_t* scnt = reinterpret_cast<uint32_t*>(cqueue);                             // [64]
                 unsigned long long* sbase = reinterpret_cast<unsigned long long*>(scnt + kQPass);  // [64]
-                uint32_t* hist_s = reinterpret_cast<uint32_t*>(sbase + kQPass);  // [64][kBins]
+                uint32_t* hist_s = reinterpret_cast<uint32_t*>(sbase + kQPass);                    // [64][kBins]
                 const uint32_t nt = *tcount;
-                if (et < kQPass) scnt[et] = 0;
-                for (uint32_t k2 = et; k2 < kQPass * kBins; k2 += 256) hist_s[k2] = 0;
-                named_bar(kEpiBar, 256);
+                if (wt < kQPass) scnt[wt] = 0;
+                for (uint32_t k2 = wt; k2 < kQPass * kBins; k2 += n_workers) hist_s[k2] = 0;
+                named_bar(kAllBar, n_workers);
                 auto survivor = [&](uint32_t ent, uint32_t& q, uint64_t& slot, int32_t& a, double& sc) {
                     const uint32_t key = st_key[ent];
                     q = ent / sw;
@@ -1027,20 +928,20 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
                     return sc >= theta_s[q];  // theta may have risen since the entry was set
                 };
-                for (uint32_t k2 = et; k2 < nt; k2 += 256) {
+                for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
                     uint32_t q;
                     uint64_t slot;
                     int32_t a;
                     double sc;
                     if (survivor(touched[k2], q, slot, a, sc)) atomicAdd(scnt + q, 1u);
                 }
-                named_bar(kEpiBar, 256);
-                if (et < p.nq) {
-                    sbase[et] = scnt[et] ? atomicAdd(p.surv_count + p.q0 + et, (unsigned long long)scnt[et]) : 0ull;
-                    scnt[et] = 0;
+                named_bar(kAllBar, n_workers);
+                if (wt < p.nq) {
+                    sbase[wt] = scnt[wt] ? atomicAdd(p.surv_count + p.q0 + wt, (unsigned long long)scnt[wt]) : 0ull;
+                    scnt[wt] = 0;
                 }
-                named_bar(kEpiBar, 256);
-                for (uint32_t k2 = et; k2 < nt; k2 += 256) {
+                named_bar(kAllBar, n_workers);
+                for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
                     const uint32_t ent = touched[k2];
                     uint32_t q;
                     uint64_t slot;
@@ -1065,19 +966,12 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     fb = fb < 0.0 ? 0.0 : (fb > double(kBins - 1) ? double(kBins - 1) : fb);
                     atomicAdd(hist_s + q * kBins + int(fb), 1u);
                 }
-                named_bar(kEpiBar, 256);
-                for (uint32_t k2 = et; k2 < p.nq * kBins; k2 += 256)
+                named_bar(kAllBar, n_workers);
+                for (uint32_t k2 = wt; k2 < p.nq * kBins; k2 += n_workers)
                     if (hist_s[k2]) atomicAdd(p.hist + uint64_t(p.q0) * kBins + k2, hist_s[k2]);
-                if (et == 0) *tcount = 0;
-                named_bar(kEpiBar, 256);
+                if (wt == 0) *tcount = 0;
+                named_bar(kAllBar, n_workers);
             }
-#ifdef RBE_PHASE_PROF
-            const long long e2c = clock64();
-            if (p.prof && et == 32) {
-                p.prof[uint64_t(1024 + blockIdx.x) * 8 + 3] += e1c - e0c;
-                p.prof[uint64_t(1024 + blockIdx.x) * 8 + 4] += e2c - e1c;
-            }
-#endif
             // ---- dynamic theta (one thread per query): raise theta_q to the lower edge of the
             // highest histogram bin whose suffix count of emitted survivors reaches n (a valid
             // lower bound on the final n-th survivor score: every emitted survivor is the final
@@ -1087,8 +981,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 int32_t* xw = xcoef + (sidx & 1) * 3 * kQPass;
                 uint8_t* xbw = xsm + (sidx & 1) * p.n_pad * 32;
                 bool ok16 = true;
-                if (et < p.nq) {
-                    const uint32_t q = et;
+                if (wt < p.nq) {
+                    const uint32_t q = wt;
                     const uint32_t* hp = p.hist + uint64_t(p.q0 + q) * kBins;
                     uint64_t suffix = 0;
                     int B = -1;
@@ -1114,19 +1008,12 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     write_xrow(xbw, p.n_pad, 0, q, x);
                     ok16 = p.f16max != 0 && x.c <= 32767 - p.f16max;
                 }
-                ok16 = __syncthreads_and_named(ok16);
-                if (et == 0) p16ok[sidx & 1] = ok16 ? 1u : 0u;
+                ok16 = bar_and(ok16, n_workers);
+                if (wt == 0) p16ok[sidx & 1] = ok16 ? 1u : 0u;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                named_bar(kEpiBar, 256);
-                if (et == 0) mbar_arrive(x_ready + (sidx & 1));
-#ifdef RBE_PHASE_PROF
-                if (p.prof && et == 32) p.prof[uint64_t(1024 + blockIdx.x) * 8 + 6] += clock64() - e2c;
-#endif
+                named_bar(kAllBar, n_workers);
+                if (wt == 0) mbar_arrive(x_ready + (sidx & 1));
             }
-#ifdef RBE_PHASE_PROF
-            RBE_CLK(c4);
-            t_end += c4 - c3;
-#endif
         }
         if (!PROBE) {
             unsigned long long sc64 = (unsigned long long)scored * p.nq, cd64 = cands;
@@ -1139,17 +1026,6 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 atomicAdd(p.candidates, cd64);
             }
         }
-#ifdef RBE_PHASE_PROF
-        if (p.prof && lane == 0 && warp == 9) {
-            unsigned long long* pr = p.prof + uint64_t(blockIdx.x) * 8;
-            pr[0] += t_wait;
-            pr[1] += t_work;
-            pr[2] += t_end;
-            pr[6] += t_ld;
-            pr[7] += t_red;
-            pr[5] += 1;
-        }
-#endif
     }
     tc_fence_before();
     __syncthreads();
@@ -1330,10 +1206,10 @@ void dispatch(uint32_t kp, bool rw, const TensorParams& tp, size_t smem, int gri
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-// TMEM: kSlots A operands (K = 32 (w32 + 1) bytes) and kSlots accumulators of 64 columns
-uint32_t pick_slots(uint32_t w32) {
-    for (uint32_t n = kSlots; n >= 2; n -= 2)
-        if (n * (8 * (w32 + 1) + kQPass) <= 512) return n;
+// TMEM: per warpgroup two A operands (K = 32 (w32 + 1) bytes) and one 64-column accumulator
+uint32_t pick_nwg(uint32_t w32) {
+    for (uint32_t n = kMaxWG; n >= 2; --n)
+        if (n * (2 * 8 * (w32 + 1) + kQPass) <= 512) return n;
     return 0;
 }
 
@@ -1391,7 +1267,7 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
     if (s.rw ? qp > 6 : qp > 63) return no("query planes exceed the s8 operand range");
     if (s.wpp > 4) return no("dim > 256");
     if (Q == 0) return no("no queries");
-    if (!pick_slots(s.w32)) return no("tensor memory");
+    if (!pick_nwg(s.w32)) return no("tensor memory");
     if (pick_stages(s.kp, s.w32, strip_width(g)) == 0) return no("shared memory");
     if (pick_lam_shift(s, qp) < 0) return no("accumulator range exceeds the threshold block");
     if (g.items_per_thread >= 511) return no("items_per_thread >= 511 (state key)");
@@ -1470,7 +1346,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.ipt = a.ipt;
     tp.w32 = s.w32;
     tp.sw = strip_width(g_of(a));
-    tp.nslots = pick_slots(s.w32);
+    tp.nwg = pick_nwg(s.w32);
     if (const char* e = getenv("RBE_DBG")) tp.dbg = uint32_t(atoi(e));
     {
         // D_sigma <= sigma * vmax * K * rqmax; the packed epilogue is used per strip when every live
@@ -1514,7 +1390,12 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
         tp.bimg = bimg + size_t(ps) * pass_bytes;
         // probe pass -> theta
         tp.probe_tiles = plan.probe_tiles;
-        dispatch<true>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
+        {
+            // probe: a warpgroup's lanes must always hold the same logical threads (nwg = spt)
+            TensorParams pp = tp;
+            if (tp.sw > 128) pp.nwg = 2;
+            dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
+        }
         const size_t tsm = size_t(kThetaCap) * 4;
         RBE_CK(cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsm)));
         theta_kernel<<<tp.nq, 1024, tsm, st>>>(probe + uint64_t(tp.q0) * per_query, per_query, plan.n, tp.L,
