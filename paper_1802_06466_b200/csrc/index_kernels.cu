@@ -69,33 +69,59 @@ __device__ __forceinline__ uint32_t unpermute_word(uint32_t dev, const uint8_t* 
     return n;
 }
 
-// natural [kp][count][wpp] u64  ->  device [kp][count_pad][W32] u32 (permuted)
+// natural [kp][count][wpp] u64  ->  device [kp][count_pad][W32] u32 (permuted;
+// plane-interleaved for kp = 3 weighted).  One thread per (doc, u32 word).
 __global__ void repack_kernel(const uint64_t* __restrict__ nat, uint32_t* __restrict__ dev, uint64_t count,
-                              uint64_t count_pad, uint32_t kp, uint32_t wpp, PlanePerm perm) {
+                              uint64_t count_pad, uint32_t kp, uint32_t wpp, uint32_t rw, PlanePerm perm) {
     const uint32_t w32 = 2 * wpp;
-    const uint64_t total = uint64_t(kp) * count * w32;
+    const uint64_t total = count * w32;
+    const bool il = interleaved_store(int(kp), rw != 0);
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total;
          e += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t g = uint32_t(e % w32);
-        const uint64_t doc = (e / w32) % count;
-        const uint32_t t = uint32_t(e / (uint64_t(w32) * count));
-        const uint32_t nw = natural_half(nat + uint64_t(t) * count * wpp, doc, g, wpp);
-        dev[(uint64_t(t) * count_pad + doc) * w32 + g] = permute_word(nw, perm.perm[t]);
+        const uint64_t doc = e / w32;
+        if (il) {
+            uint32_t w[3], z[3];
+            for (uint32_t t = 0; t < 3; ++t)
+                w[t] = permute_word(natural_half(nat + uint64_t(t) * count * wpp, doc, g, wpp), perm.perm[t]);
+            interleave3(w, z);
+            for (uint32_t t = 0; t < 3; ++t) dev[(uint64_t(t) * count_pad + doc) * w32 + g] = z[t];
+        } else {
+            for (uint32_t t = 0; t < kp; ++t) {
+                const uint32_t nw = natural_half(nat + uint64_t(t) * count * wpp, doc, g, wpp);
+                dev[(uint64_t(t) * count_pad + doc) * w32 + g] = permute_word(nw, perm.perm[t < uint32_t(kMaxPlanes) ? t : 0]);
+            }
+        }
     }
 }
 
 __global__ void unpack_kernel(const uint32_t* __restrict__ dev, uint64_t* __restrict__ nat, uint64_t count,
-                              uint64_t count_pad, uint32_t kp, uint32_t wpp, PlanePerm perm) {
-    const uint64_t total = uint64_t(kp) * count * wpp;
+                              uint64_t count_pad, uint32_t kp, uint32_t wpp, uint32_t rw, PlanePerm perm) {
+    const uint64_t total = count * wpp;
+    const uint32_t w32 = 2 * wpp;
+    const bool il = interleaved_store(int(kp), rw != 0);
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total;
          e += uint64_t(gridDim.x) * blockDim.x) {
         const uint32_t w = uint32_t(e % wpp);
-        const uint64_t doc = (e / wpp) % count;
-        const uint32_t t = uint32_t(e / (uint64_t(wpp) * count));
-        const uint32_t* src = dev + (uint64_t(t) * count_pad + doc) * (2 * wpp) + 2 * w;
-        const uint64_t lo = unpermute_word(src[0], perm.perm[t]);
-        const uint64_t hi = unpermute_word(src[1], perm.perm[t]);
-        nat[(uint64_t(t) * count + doc) * wpp + w] = lo | (hi << 32);
+        const uint64_t doc = e / wpp;
+        for (uint32_t t = 0; t < kp; ++t) {
+            uint32_t lo, hi;
+            if (il) {
+                uint32_t z[3], pw[3];
+                for (uint32_t c = 0; c < 3; ++c) z[c] = dev[(uint64_t(c) * count_pad + doc) * w32 + 2 * w];
+                deinterleave3(z, pw);
+                lo = pw[t];
+                for (uint32_t c = 0; c < 3; ++c) z[c] = dev[(uint64_t(c) * count_pad + doc) * w32 + 2 * w + 1];
+                deinterleave3(z, pw);
+                hi = pw[t];
+            } else {
+                const uint32_t* src = dev + (uint64_t(t) * count_pad + doc) * w32 + 2 * w;
+                lo = src[0];
+                hi = src[1];
+            }
+            const uint8_t* pm = perm.perm[t < uint32_t(kMaxPlanes) ? t : 0];
+            nat[(uint64_t(t) * count + doc) * wpp + w] = uint64_t(unpermute_word(lo, pm)) | (uint64_t(unpermute_word(hi, pm)) << 32);
+        }
     }
 }
 
@@ -131,6 +157,14 @@ __global__ void fill_synthetic_kernel(uint32_t* __restrict__ planes, float* __re
                 for (int b = 0; b < 64; ++b) x[b] = __dadd_rn(x[b], ((v >> b) & 1) ? wt : -wt);
             }
             for (uint32_t b = 0; b < nbits; ++b) sq = __dadd_rn(sq, __dmul_rn(x[b], x[b]));
+        }
+        if (interleaved_store(int(kp), rw != 0)) {
+            for (uint32_t g = 0; g < w32; ++g) {
+                uint32_t w[3], z[3];
+                for (uint32_t t = 0; t < 3; ++t) w[t] = planes[(uint64_t(t) * count_pad + s) * w32 + g];
+                interleave3(w, z);
+                for (uint32_t t = 0; t < 3; ++t) planes[(uint64_t(t) * count_pad + s) * w32 + g] = z[t];
+            }
         }
         mags[s] = __double2float_rn(__dsqrt_rn(sq));
         ids[s] = gdoc;
@@ -174,16 +208,16 @@ __global__ void fill_f32_kernel(float* p, uint64_t n, float v) {
 void launch_repack_planes(const uint64_t* d_natural, uint32_t* d_dev, uint64_t count, uint64_t count_pad,
                           const Shape& s, const PlanePerm& perm, cudaStream_t st) {
     if (count == 0) return;
-    repack_kernel<<<grid_for(uint64_t(s.kp) * count * s.w32), kThreads, 0, st>>>(d_natural, d_dev, count, count_pad,
-                                                                               s.kp, s.wpp, perm);
+    repack_kernel<<<grid_for(count * s.w32), kThreads, 0, st>>>(d_natural, d_dev, count, count_pad, s.kp, s.wpp, s.rw,
+                                                               perm);
     RBE_CK(cudaGetLastError());
 }
 
 void launch_unpack_planes(const uint32_t* d_dev, uint64_t* d_natural, uint64_t count, uint64_t count_pad,
                           const Shape& s, const PlanePerm& perm, cudaStream_t st) {
     if (count == 0) return;
-    unpack_kernel<<<grid_for(uint64_t(s.kp) * count * s.wpp), kThreads, 0, st>>>(d_dev, d_natural, count, count_pad,
-                                                                                s.kp, s.wpp, perm);
+    unpack_kernel<<<grid_for(count * s.wpp), kThreads, 0, st>>>(d_dev, d_natural, count, count_pad, s.kp, s.wpp, s.rw,
+                                                              perm);
     RBE_CK(cudaGetLastError());
 }
 

@@ -137,6 +137,46 @@ struct Expand<4, true> {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Plane interleaving (kp = 3, residual weights).  The store keeps, per 32-dim
+// group, the three (permuted) plane words pre-merged as z_c, c = 0..2:
+//   z0 = w0 @ 0x24.. | w1 @ 0x92.. | w2 @ 0x49..
+//   z1 = w0 @ 0x49.. | w1 @ 0x24.. | w2 @ 0x92..
+//   z2 = w0 @ 0x92.. | w1 @ 0x49.. | w2 @ 0x24..
+// (a bijection of the same 96 bits: every bit position takes each plane once
+// across z0..z2).  These are exactly the merged words Expand<3, true> builds
+// first, so the tensor scan expands straight from the stored words.
+__host__ __device__ __forceinline__ constexpr bool interleaved_store(int kp, bool rw) { return kp == 3 && rw; }
+__host__ __device__ __forceinline__ void interleave3(const uint32_t* w, uint32_t* z) {
+    z[0] = sel32(0x24242424u, w[0], sel32(0x92929292u, w[1], w[2]));
+    z[1] = sel32(0x49494949u, w[0], sel32(0x24242424u, w[1], w[2]));
+    z[2] = sel32(0x92929292u, w[0], sel32(0x49494949u, w[1], w[2]));
+}
+__host__ __device__ __forceinline__ void deinterleave3(const uint32_t* z, uint32_t* w) {
+    w[0] = (z[0] & 0x24242424u) | (z[1] & 0x49494949u) | (z[2] & 0x92929292u);
+    w[1] = (z[0] & 0x92929292u) | (z[1] & 0x24242424u) | (z[2] & 0x49494949u);
+    w[2] = (z[0] & 0x49494949u) | (z[1] & 0x92929292u) | (z[2] & 0x24242424u);
+}
+
+// Expansion from the STORED words of a 32-dim group (interleaved for kp = 3 weighted).
+template <int KP, bool RW>
+struct ExpandStored {
+    __host__ __device__ __forceinline__ static void run(const uint32_t* w, uint32_t* out) { Expand<KP, RW>::run(w, out); }
+};
+template <>
+struct ExpandStored<3, true> {
+    __host__ __device__ __forceinline__ static void run(const uint32_t* z, uint32_t* out) {
+        out[0] = z[0] & 0x07070707u;
+        out[1] = shr(z[0], 3) & 0x07070707u;
+        out[2] = shr(z[1], 1) & 0x07070707u;
+        out[3] = shr(z[1], 4) & 0x07070707u;
+        out[4] = shr(z[2], 2) & 0x07070707u;
+        out[5] = shr(z[2], 5) & 0x07070707u;
+        out[6] = (shr(z[0], 6) & 0x03030303u) | (shl(z[1], 2) & 0x04040404u);
+        out[7] = (shr(z[1], 7) & 0x01010101u) | (shl(z[2], 1) & 0x06060606u);
+    }
+};
+
 // Runtime-dispatched host version (permutation derivation, tests).
 inline void expand32_host(int kp, bool rw, const uint32_t* w, uint32_t* out) {
     if (rw) {

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kThreads) scan_exact_kernel(ScanArgs a, uint32
             int64_t acc[QG];
 #pragma unroll
             for (int j = 0; j < QG; ++j) acc[j] = 0;
+            const bool il = interleaved_store(int(kp), rw != 0);
             for (uint32_t t = 0; t < kp; ++t) {
                 const uint32_t* dw = part.planes + (uint64_t(t) * part.count_pad + z) * w32;
                 for (uint32_t s = 0; s < qp; ++s) {
@@ -102,7 +103,16 @@ __global__ void __launch_bounds__(kThreads) scan_exact_kernel(ScanArgs a, uint32
 #pragma unroll
                     for (int j = 0; j < QG; ++j) mism[j] = 0;
                     for (uint32_t g = 0; g < w32; ++g) {
-                        const uint32_t d = __ldg(dw + g);
+                        uint32_t d;
+                        if (il) {  // plane-interleaved store: recover plane t's word of group g
+                            uint32_t zz[3], pw[3];
+                            for (uint32_t c = 0; c < 3; ++c)
+                                zz[c] = __ldg(part.planes + (uint64_t(c) * part.count_pad + z) * w32 + g);
+                            deinterleave3(zz, pw);
+                            d = pw[t];
+                        } else {
+                            d = __ldg(dw + g);
+                        }
 #pragma unroll
                         for (int j = 0; j < QG; ++j) mism[j] += __popc(sq[((j * kp + t) * qp + s) * w32 + g] ^ d);
                     }

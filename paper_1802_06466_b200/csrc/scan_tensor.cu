@@ -63,9 +63,8 @@ namespace {
 
 constexpr int kStages = 12;          // max ring depth (stages of sw docs)
 constexpr int kMaxWG = 3;            // worker warpgroups
-constexpr int kThreads = 512;        // 16 warps (roles: see tensor_scan_kernel), 128 registers each
+constexpr int kThreads = 416;        // 13 warps (roles: see tensor_scan_kernel), 128 registers each
 constexpr int kProducerWarp = 12;
-constexpr int kMmaWarp0 = 13;        // one MMA issuer warp per worker warpgroup
 constexpr uint32_t kCandQueue = 4096;  // deferred candidates per strip (shared memory; overflow is scored at once)
 constexpr int kAllBar = 8;           // named barrier of all worker threads
 constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
@@ -439,7 +438,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uin
     s.qconst = off;
     off = al(off + kQPass * 8 + kQPass * 4 + 2 * 3 * kQPass * 4 + 16);
     s.bars = off;
-    off = al(off + (2 * nstages + 2 * kMaxWG + 2) * 8 + 32);
+    off = al(off + (2 * nstages + 2 * kMaxWG + 2) * 8 + 64);
     s.total = off;
     return s;
 }
@@ -475,14 +474,24 @@ __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, ui
     }
 }
 
-// Warp roles (16 warps, 128 registers each):
+// Warp roles (13 warps, 128 registers each):
 //   warps 0..4*nwg-1   workers: warpgroup w = warp/4 takes sub-tiles u = w (mod nwg)
 //                      (128 docs, CTA-local counter u); quadrant warp%4 = TMEM lanes.
 //                      Per warpgroup, software-pipelined within a strip:
 //                        expand(k+1) -> A[(k+1)&1] while the tensor core runs MMA(k);
-//                        wait MMA(k); test D; arrive a_full (A(k+1) ready, D free)
+//                        wait MMA(k); test D; the last warp of the four to finish issues
+//                        MMA(k+1) (A(k+1) ready, D free)
 //   warp 12            producer: one contiguous sw-doc stage per tile; TMEM allocator
-//   warps 13..13+nwg-1 MMA issuers, one per warpgroup (whole warp, elected lane)
+// phase timing of the worker loop (build with RBE_NVCC_EXTRA=-DRBE_PHASE_PROF, run with RBE_PROF=1)
+#ifdef RBE_PHASE_PROF
+#define RBE_CLK(x) const long long x = clock64()
+#define RBE_ACC(slot, v) \
+    if (p.prof && lane == 0 && warp == 1) p.prof[uint64_t(blockIdx.x) * 8 + (slot)] += (v)
+#else
+#define RBE_CLK(x)
+#define RBE_ACC(slot, v)
+#endif
+
 template <int KP, bool RW, bool PROBE>
 __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -516,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_ready + 2);
     uint32_t* cq_count = tmem_slot + 1;
     uint32_t* tcount = tmem_slot + 2;
+    uint32_t* wg_arrivals = tmem_slot + 4;  // [kMaxWG] per-warpgroup arrival counters (MMA issue)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -565,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
         mbar_init(x_ready + 1, 1);
         *cq_count = 0;
         *tcount = 0;
+        for (int w = 0; w < kMaxWG; ++w) wg_arrivals[w] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kProducerWarp) {
@@ -597,41 +608,6 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                                  plane_bytes, full + rs.idx);
                     bulk_g2s(dst + KP * plane_bytes, part.mags + slot0, sw * 4, full + rs.idx);
                 }
-            }
-        }
-    } else if (warp >= kMmaWarp0 && warp < kMmaWarp0 + int(nwg)) {
-        // ===================== MMA issuer of warpgroup w (whole warp, one elected lane issues) =====================
-        const uint32_t w = uint32_t(warp - kMmaWarp0);
-        const uint32_t idesc = idesc_i8(128, p.n_pad);
-        const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
-        const uint64_t x_desc0 = smem_desc(smem_u32(xsm));
-        const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
-        const uint32_t a_base = tmem_base + w * wg_cols;
-        const uint32_t d_t = a_base + 2 * a_cols;
-        uint32_t c = 0, u0 = 0, sidx = 0;
-        for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
-            const StripInfo si = strip_info(p, s);
-            const uint32_t n_sub = si.n_tiles * spt;
-            const uint32_t first = (w + nwg - u0 % nwg) % nwg;
-            const uint32_t mine = n_sub > first ? (n_sub - first + nwg - 1) / nwg : 0;
-            u0 += n_sub;
-            if (!PROBE && sidx >= 2 && mine > 0) {
-                // X block of parity sidx&1 was rewritten at the end of strip sidx-2
-                mbar_wait_sleep(x_ready + (sidx & 1), ((sidx - 2) >> 1) & 1);
-            }
-            const uint64_t xd = x_desc0 + (sidx & 1) * b_step;
-            for (uint32_t k = 0; k < mine; ++k, ++c) {
-                mbar_wait_sleep(a_full + w, c & 1);
-                tc_fence_after();
-                const uint32_t a_t = a_base + (c & 1) * a_cols;
-                switch (w32) {
-                    case 2: mma_group<2>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                    case 4: mma_group<4>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                    case 6: mma_group<6>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                    default: mma_group<8>(d_t, a_t, b_desc0, b_step, xd, idesc); break;
-                }
-                mma_commit_elect(mma_done + w);
-                __syncwarp();
             }
         }
     } else if (warp < int(4 * nwg)) {
@@ -676,11 +652,11 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         w3[t] = v.w;
                     }
                     uint32_t out[16];
-                    Expand<KP, RW>::run(w0, out);
-                    Expand<KP, RW>::run(w1, out + 8);
+                    ExpandStored<KP, RW>::run(w0, out);
+                    ExpandStored<KP, RW>::run(w1, out + 8);
                     tmem_st16(a_t + 32 * g4, out);
-                    Expand<KP, RW>::run(w2, out);
-                    Expand<KP, RW>::run(w3, out + 8);
+                    ExpandStored<KP, RW>::run(w2, out);
+                    ExpandStored<KP, RW>::run(w3, out + 8);
                     tmem_st16(a_t + 32 * g4 + 16, out);
                 }
             } else {
@@ -695,8 +671,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         w1[t] = v.y;
                     }
                     uint32_t out[16];
-                    Expand<KP, RW>::run(w0, out);
-                    Expand<KP, RW>::run(w1, out + 8);
+                    ExpandStored<KP, RW>::run(w0, out);
+                    ExpandStored<KP, RW>::run(w1, out + 8);
                     tmem_st16(a_t + 16 * g2, out);
                 }
             }
@@ -706,12 +682,40 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + st);  // this warp's share of the stage is consumed
         };
-        // this warp's part of A is complete and its D reads are done: one arrival per warp
-        auto arrive_a = [&]() {
+        // This warp's part of A(k) is complete and its reads of D are done.  The last of the
+        // warpgroup's four warps to get here issues MMA(k) (whole warp, one elected lane), so no
+        // warp ever waits for an issuer: the per-warpgroup counter in shared memory orders it.
+        const uint32_t idesc = idesc_i8(128, p.n_pad);
+        const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
+        const uint64_t x_desc0 = smem_desc(smem_u32(xsm));
+        const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
+        const uint32_t a_w = tmem_base + wg * wg_cols;         // lane 0 of this warpgroup's A[0]
+        const uint32_t d_w = a_w + 2 * a_cols;
+        uint32_t xpar = 0;  // X block parity of the current strip
+        auto arrive_a = [&](uint32_t ab) {
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(a_full + wg);
+            uint32_t old = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                old = atomicAdd(wg_arrivals + wg, 1u);
+            }
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if ((old & 3u) == 3u) {
+                __threadfence_block();
+                tc_fence_after();
+                const uint32_t a_t = a_w + ab * a_cols;
+                const uint64_t xd = x_desc0 + xpar * b_step;
+                switch (w32) {
+                    case 2: mma_group<2>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
+                    case 4: mma_group<4>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
+                    case 6: mma_group<6>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
+                    default: mma_group<8>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
+                }
+                mma_commit_elect(mma_done + wg);
+                __syncwarp();
+            }
         };
 
         uint32_t u0 = 0, tiles0 = 0, sidx = 0;
@@ -722,6 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             const uint64_t lim = part.count > si.base ? part.count - si.base : 0;  // valid: i*tpb + col < lim
             const int32_t* xc = xcoef + (sidx & 1) * 3 * kQPass;
             const bool p16 = p16ok[sidx & 1] != 0;
+            xpar = sidx & 1;
             uint32_t k = (wg + nwg - u0 % nwg) % nwg;
             if (k < n_sub) {
                 uint32_t ti = k >> spt_sh;
@@ -738,21 +743,26 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 uint32_t col = (k & (spt - 1)) * 128 + l, col_n = 0;
                 mbar_wait(full + st_idx, st_ph);
                 expand(st_idx, col, kc & 1, mag, j);
-                arrive_a();
+                arrive_a(kc & 1);
                 while (true) {
                     const uint32_t k_n = k + nwg;
                     const bool has_next = k_n < n_sub;
                     const uint32_t i = k >> spt_sh;
+                    RBE_CLK(c0);
                     if (has_next) {
                         seek(k_n >> spt_sh);
                         col_n = (k_n & (spt - 1)) * 128 + l;
                         mbar_wait(full + st_idx, st_ph);
+                        RBE_CLK(c0b);
+                        RBE_ACC(0, c0b - c0);
                         expand(st_idx, col_n, (kc + 1) & 1, mag_n, j_n);
                     }
+                    RBE_CLK(c1);
                     const bool valid = uint64_t(i) * p.tpb + col < lim;
                     scored += valid ? 1 : 0;
                     mbar_wait_sleep(mma_done + wg, kc & 1);
                     tc_fence_after();
+                    RBE_CLK(c2);
                     if (PROBE) {
                         // F = lambda acc; per-thread maxima of the (float) score
                         const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
@@ -835,8 +845,13 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         }
                     }
                     ++kc;
+                    RBE_CLK(c3);
+                    RBE_ACC(1, c1 - c0);
+                    RBE_ACC(2, c2 - c1);
+                    RBE_ACC(3, c3 - c2);
+                    RBE_ACC(5, 1);
                     if (!has_next) break;
-                    arrive_a();  // A(k+nwg) ready, D read: the MMA warp may issue
+                    arrive_a(kc & 1);  // A(k+nwg) ready (kc already advanced), D read
                     k = k_n;
                     col = col_n;
                     mag = mag_n;
@@ -846,6 +861,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             }
             u0 += n_sub;
             tiles0 += si.n_tiles;
+            RBE_CLK(c4);
             // ================= strip end (all worker threads) =================
             if (PROBE) {
                 // merge the warpgroups' per-lane maxima: the lanes of warpgroup w always hold
@@ -976,10 +992,11 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             // highest histogram bin whose suffix count of emitted survivors reaches n (a valid
             // lower bound on the final n-th survivor score: every emitted survivor is the final
             // per-thread best of a distinct logical thread), then rewrite the X block of parity
-            // sidx&1, used next by strip sidx+2 (whose MMAs wait for x_ready).
+            // (sidx+1)&1 for the next strip (no MMA is in flight: the workers issue them and
+            // are all here).
             {
-                int32_t* xw = xcoef + (sidx & 1) * 3 * kQPass;
-                uint8_t* xbw = xsm + (sidx & 1) * p.n_pad * 32;
+                int32_t* xw = xcoef + ((sidx + 1) & 1) * 3 * kQPass;
+                uint8_t* xbw = xsm + ((sidx + 1) & 1) * p.n_pad * 32;
                 bool ok16 = true;
                 if (wt < p.nq) {
                     const uint32_t q = wt;
@@ -1009,11 +1026,12 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     ok16 = p.f16max != 0 && x.c <= 32767 - p.f16max;
                 }
                 ok16 = bar_and(ok16, n_workers);
-                if (wt == 0) p16ok[sidx & 1] = ok16 ? 1u : 0u;
+                if (wt == 0) p16ok[(sidx + 1) & 1] = ok16 ? 1u : 0u;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 named_bar(kAllBar, n_workers);
-                if (wt == 0) mbar_arrive(x_ready + (sidx & 1));
             }
+            RBE_CLK(c5);
+            RBE_ACC(4, c5 - c4);
         }
         if (!PROBE) {
             unsigned long long sc64 = (unsigned long long)scored * p.nq, cd64 = cands;
@@ -1410,25 +1428,15 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
         dispatch<false>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, false).total, grid, st);
         tp.prof = nullptr;
         if (prof) {
-            std::vector<unsigned long long> h(size_t(2048) * 8);
+            std::vector<unsigned long long> h(size_t(grid) * 8);
             RBE_CK(cudaMemcpyAsync(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost, st));
             RBE_CK(cudaStreamSynchronize(st));
-            {
-                double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int b = 0; b < grid; ++b)
-                    for (int k = 0; k < 8; ++k) m[k] += double(h[size_t(1024 + b) * 8 + k]);
-                fprintf(stderr, "[rbe prof] MMA warp 0 per sub-tile: waiting for A %.0f, for D free %.0f, issuing %.0f cycles\n",
-                        m[0] / m[5], m[1] / m[5], m[2] / m[5]);
-                fprintf(stderr, "[rbe prof] strip ends per CTA: candidates %.0f, emission %.0f, theta refresh %.0f cycles\n",
-                        m[3] / grid, m[4] / grid, m[6] / grid);
-            }
             double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (int b = 0; b < grid; ++b)
                 for (int k = 0; k < 8; ++k) acc[k] += double(h[size_t(b) * 8 + k]);
-            fprintf(stderr, "[rbe prof] per CTA: epilogue warp waiting for D %.0f cycles, testing %.0f, strip ends %.0f; "
-                            "expand warp waiting %.0f, expanding %.0f; epilogue: ld %.0f, ld+reduce %.0f\n",
-                    acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[4] / acc[5],
-                    acc[6] / acc[5], acc[7] / acc[5]);
+            fprintf(stderr, "[rbe prof] worker warp per sub-tile: wait full %.0f, expand(+wait) %.0f, wait MMA %.0f, test %.0f; "
+                            "strip ends %.0f per CTA (n=%.0f)\n",
+                    acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[4] / grid, acc[5]);
         }
         launches += 3;
     }
