@@ -16,7 +16,8 @@ namespace rbe_dev {
 namespace {
 
 constexpr int kThreads = 1024;
-constexpr uint32_t kCap = 8192;  // keys sorted in shared memory
+constexpr uint32_t kCap = 8192;    // keys sorted in shared memory
+constexpr uint32_t kSmall = 2048;  // direct sort / radix-select stop size (bitonic cost grows as m log^2 m)
 
 struct Key {
     uint64_t hi, lo;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) select_topn_kernel(const Result* __r
     }
     if (n_eff == 0) return;
 
-    if (m <= kCap) {
+    if (m <= kSmall) {
         uint32_t n2 = 1;
         while (n2 < m) n2 <<= 1;
         for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) select_topn_kernel(const Result* __r
             s_nd = d + 1;
         }
         __syncthreads();
-        if (s_bkt <= kCap) break;
+        if (s_bkt <= kSmall) break;
     }
     const int nd = s_nd;
     const uint64_t ph = s_ph, pl = s_pl, r = s_r;
