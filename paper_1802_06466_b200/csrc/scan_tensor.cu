@@ -485,8 +485,7 @@ __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, ui
 // phase timing of the worker loop (build with RBE_NVCC_EXTRA=-DRBE_PHASE_PROF, run with RBE_PROF=1)
 #ifdef RBE_PHASE_PROF
 #define RBE_CLK(x) const long long x = clock64()
-#define RBE_ACC(slot, v) \
-    if (p.prof && lane == 0 && warp == 1) p.prof[uint64_t(blockIdx.x) * 8 + (slot)] += (v)
+#define RBE_ACC(slot, v) prof_acc[slot] += (v)
 #else
 #define RBE_CLK(x)
 #define RBE_ACC(slot, v)
@@ -622,6 +621,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
         const uint32_t pstride = p.ptop;
         uint32_t scored = 0, cands = 0;
         uint32_t kc = 0;  // sub-tiles processed by this warpgroup (A buffer / barrier parities)
+#ifdef RBE_PHASE_PROF
+        long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // registers: flushed once at the end
+#endif
         float pm[PROBE ? kQPass : 1];
 #pragma unroll
         for (int e = 0; e < (PROBE ? kQPass : 1); ++e) pm[e] = -INFINITY;
@@ -697,13 +699,13 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             tc_fence_before();
             __syncwarp();
             uint32_t old = 0;
-            if (lane == 0) {
-                __threadfence_block();
-                old = atomicAdd(wg_arrivals + wg, 1u);
-            }
+            if (lane == 0)  // acq_rel: publishes this warp's A, acquires the others' for the last arriver
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(old)
+                             : "r"(smem_u32(wg_arrivals + wg))
+                             : "memory");
             old = __shfl_sync(0xffffffffu, old, 0);
             if ((old & 3u) == 3u) {
-                __threadfence_block();
                 tc_fence_after();
                 const uint32_t a_t = a_w + ab * a_cols;
                 const uint64_t xd = x_desc0 + xpar * b_step;
@@ -993,8 +995,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             // lower bound on the final n-th survivor score: every emitted survivor is the final
             // per-thread best of a distinct logical thread), then rewrite the X block of parity
             // (sidx+1)&1 for the next strip (no MMA is in flight: the workers issue them and
-            // are all here).
-            {
+            // are all here).  theta converges within the first strips; later refreshes are
+            // spaced out (a stale X block only means a lower, still valid, threshold).
+            if (sidx < 4 || (sidx & 3) == 3) {
                 int32_t* xw = xcoef + ((sidx + 1) & 1) * 3 * kQPass;
                 uint8_t* xbw = xsm + ((sidx + 1) & 1) * p.n_pad * 32;
                 bool ok16 = true;
@@ -1033,6 +1036,10 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             RBE_CLK(c5);
             RBE_ACC(4, c5 - c4);
         }
+#ifdef RBE_PHASE_PROF
+        if (p.prof && lane == 0 && warp == 1)
+            for (int k2 = 0; k2 < 8; ++k2) p.prof[uint64_t(blockIdx.x) * 8 + k2] += prof_acc[k2];
+#endif
         if (!PROBE) {
             unsigned long long sc64 = (unsigned long long)scored * p.nq, cd64 = cands;
             for (int off = 16; off > 0; off >>= 1) {
@@ -1303,6 +1310,7 @@ TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geom
     pl.qp = qp;
     pl.n = n;
     pl.probe_tiles = probe_tiles ? probe_tiles : 8;
+    if (const char* e = getenv("RBE_PROBE_TILES")) pl.probe_tiles = uint32_t(atoi(e));  // tuning experiments
     pl.prefix.assign(counts.size() + 1, 0);
     const uint64_t threads = uint64_t(g.blocks) * g.threads_per_block;
     for (size_t i = 0; i < counts.size(); ++i) {
