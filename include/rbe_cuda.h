@@ -145,12 +145,19 @@ typedef struct {
 
 /* Same search with the query batch and outputs in DEVICE memory on the
  * index's device: out = rbe_result[n_queries][n] (invalid tail entries have
- * valid = 0).  `stream` is a cudaStream_t (NULL = the index's own stream);
- * the call returns after the batch completes on that stream. */
+ * valid = 0).  `stream` is a cudaStream_t (NULL = the index's own stream).
+ * With `stats` non-NULL the call returns after the batch completes on that
+ * stream; with `stats` NULL (and the tensor variant) it only enqueues the
+ * batch on the stream (no host synchronisation), so back-to-back batches keep
+ * the GPU busy. */
 int rbe_cuda_search_device(rbe_cuda_index* index, const uint64_t* d_query_words, uint32_t n_queries,
                            uint32_t query_planes, const rbe_scan_geometry* geometry, uint64_t n,
                            const rbe_search_options* options, rbe_result* d_out, void* stream,
                            rbe_search_stats* stats);
+
+/* Device times (ms) of the index's last batch: the scan kernels and the whole
+ * batch (CUDA events on the batch's stream); waits for that batch. */
+int rbe_cuda_index_last_batch_ms(rbe_cuda_index* index, double* scan_ms, double* total_ms);
 
 /* Merge `n_lists` result lists per query (d_in = rbe_result[n_lists][n_queries][n],
  * device memory on `device`) into the top n per query under (score desc,

@@ -169,8 +169,10 @@ struct BatchResult {
 
 // Runs one batch with queries already on the device (ix->queries) and leaves
 // rbe_result[Q][n] in ix->out.  Returns stats.
+// sync = false (tensor variant only): the whole batch is enqueued on `st` with no host
+// synchronisation (no stats; the consistency flag is checked by the next synchronous call).
 void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, const rbe_scan_geometry* g, uint64_t n,
-               const rbe_search_options* opt, rbe_search_stats* st_out) {
+               const rbe_search_options* opt, rbe_search_stats* st_out, bool sync = true) {
     const Shape& s = ix->shape;
     ScanArgs a;
     a.parts = ix->d_parts;
@@ -189,6 +191,7 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
     if (variant == RBE_VARIANT_TENSOR && !tensor_ok)
         throw InvalidArgument("search: tensor variant unsupported for this shape: " + why);
     if (variant == RBE_VARIANT_AUTO) variant = tensor_ok ? RBE_VARIANT_TENSOR : RBE_VARIANT_EXACT;
+    if (variant != RBE_VARIANT_TENSOR) sync = true;  // the exact kernel may need its overflow retry
 
     rbe_search_stats stats{};
     stats.variant = variant;
@@ -254,6 +257,7 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
                                               ix->thresholds.p, ix->queue_scratch.p, d_cands, st);
             RBE_CK(cudaEventRecord(ix->ev[2], st));
         }
+        if (!sync) break;  // the tensor kernel never sets the overflow flag
         unsigned int flags[2] = {0, 0};
         RBE_CK(cudaMemcpyAsync(flags, d_overflow, sizeof(flags), cudaMemcpyDeviceToHost, st));
         RBE_CK(cudaStreamSynchronize(st));
@@ -272,6 +276,10 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
     launch_select_topn(a.surv, a.surv_count, a.surv_cap, Q, n, ix->out.as<Result>(), ix->sel_scratch.p, ss, st);
     stats.launches += 1;
     RBE_CK(cudaEventRecord(ix->ev[3], st));
+    if (!sync) {
+        if (st_out) *st_out = stats;
+        return;
+    }
     unsigned long long host_counters[8];
     RBE_CK(cudaMemcpyAsync(host_counters, ix->counters.p, 64, cudaMemcpyDeviceToHost, st));
     std::vector<unsigned long long> sc(Q);
@@ -468,9 +476,9 @@ int rbe_cuda_search_device(rbe_cuda_index* ix, const uint64_t* d_query_words, ui
         const size_t qbytes = size_t(n_queries) * query_planes * ix->shape.wpp * 8;
         ix->queries.ensure(qbytes);
         RBE_CK(cudaMemcpyAsync(ix->queries.p, d_query_words, qbytes, cudaMemcpyDeviceToDevice, st));
-        run_batch(ix, st, n_queries, query_planes, geometry, n, options, stats);
+        run_batch(ix, st, n_queries, query_planes, geometry, n, options, stats, stats != nullptr);
         RBE_CK(cudaMemcpyAsync(d_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToDevice, st));
-        RBE_CK(cudaStreamSynchronize(st));
+        if (stats) RBE_CK(cudaStreamSynchronize(st));
     });
 }
 
@@ -512,6 +520,20 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
             }
             counts[q] = c;
         }
+    });
+}
+
+int rbe_cuda_index_last_batch_ms(rbe_cuda_index* ix, double* scan_ms, double* total_ms) {
+    return guarded([&] {
+        if (!ix) throw InvalidArgument("rbe_cuda_index_last_batch_ms: null index");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        DeviceGuard dg(ix->device);
+        RBE_CK(cudaEventSynchronize(ix->ev[3]));
+        float ms = 0;
+        RBE_CK(cudaEventElapsedTime(&ms, ix->ev[1], ix->ev[2]));
+        if (scan_ms) *scan_ms = ms;
+        RBE_CK(cudaEventElapsedTime(&ms, ix->ev[0], ix->ev[3]));
+        if (total_ms) *total_ms = ms;
     });
 }
 

@@ -313,7 +313,7 @@ PYBIND11_MODULE(_core, m) {
     m.def(
         "search_device",
         [](uintptr_t handle, uintptr_t d_words, uint32_t Q, uint32_t qp, const ScanGeometry& g, uint64_t n,
-           uintptr_t d_out, uintptr_t stream, const std::string& variant) {
+           uintptr_t d_out, uintptr_t stream, const std::string& variant, bool with_stats) {
             const rbe_scan_geometry geo{g.blocks, g.threads_per_block, g.items_per_thread, g.queue_length};
             rbe_search_options opt{};
             opt.variant = uint32_t(parse_variant(variant));
@@ -324,7 +324,7 @@ PYBIND11_MODULE(_core, m) {
                 status = rbe_cuda_search_device(reinterpret_cast<rbe_cuda_index*>(handle),
                                                 reinterpret_cast<const uint64_t*>(d_words), Q, qp, &geo, n, &opt,
                                                 reinterpret_cast<rbe_result*>(d_out),
-                                                reinterpret_cast<void*>(stream), &st);
+                                                reinterpret_cast<void*>(stream), with_stats ? &st : nullptr);
             }
             ck(status);
             py::dict d;
@@ -339,7 +339,21 @@ PYBIND11_MODULE(_core, m) {
             return d;
         },
         py::arg("handle"), py::arg("d_words"), py::arg("n_queries"), py::arg("query_planes"), py::arg("geometry"),
-        py::arg("n"), py::arg("d_out"), py::arg("stream") = 0, py::arg("variant") = "auto");
+        py::arg("n"), py::arg("d_out"), py::arg("stream") = 0, py::arg("variant") = "auto",
+        py::arg("with_stats") = true);
+    m.def(
+        "last_batch_ms",
+        [](uintptr_t handle) {
+            double scan = 0, total = 0;
+            int status;
+            {
+                py::gil_scoped_release nogil;
+                status = rbe_cuda_index_last_batch_ms(reinterpret_cast<rbe_cuda_index*>(handle), &scan, &total);
+            }
+            ck(status);
+            return py::make_tuple(scan, total);
+        },
+        py::arg("handle"));
     m.def(
         "merge_device",
         [](int device, uintptr_t d_in, uint32_t n_lists, uint32_t Q, uint64_t n, uintptr_t d_out, uintptr_t stream) {

@@ -23,7 +23,8 @@ def test_header_declares_entry_points():
     names = declared()
     for must in ("rbe_cuda_index_create", "rbe_cuda_index_upload_partition", "rbe_cuda_index_fill_synthetic",
                  "rbe_cuda_index_destroy", "rbe_cuda_search", "rbe_cuda_search_device", "rbe_cuda_merge_device",
-                 "rbe_cuda_search_multi", "rbe_cuda_last_error", "rbe_cuda_version"):
+                 "rbe_cuda_search_multi", "rbe_cuda_last_error", "rbe_cuda_version",
+                 "rbe_cuda_index_last_batch_ms"):
         assert must in names
 
 
