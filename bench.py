@@ -283,12 +283,12 @@ def run_ours(args):
     e2e = None
     if world == 1:
         for _ in range(2):
-            dix.search_words(qs, geo, K_TOP, args.variant)
+            dix.search_words(qs, geo, K_TOP, args.variant, 0, False)
         t0 = time.perf_counter()
         e2e_times = []
         for _ in range(args.steps):
             t1 = time.perf_counter()
-            dix.search_words(qs, geo, K_TOP, args.variant)
+            dix.search_words(qs, geo, K_TOP, args.variant, 0, False)
             e2e_times.append(time.perf_counter() - t1)
         e2e_total = time.perf_counter() - t0
         e2e = {"value": Q * args.steps / e2e_total, "unit": UNIT, "h2d_bytes_per_step": int(qs.nbytes),

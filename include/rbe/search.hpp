@@ -83,6 +83,12 @@ public:
                                               uint32_t query_planes, const ScanGeometry& geometry, uint64_t n,
                                               SearchStats* stats = nullptr, ScanVariant variant = ScanVariant::Auto,
                                               uint32_t probe_tiles = 0) const;
+    /// Same, writing into caller-owned [Q][n] arrays (counts[Q] valid entries per query);
+    /// stats may be null (then the batch runs with a single host synchronisation).
+    void search_words_into(std::span<const uint64_t> query_words, uint32_t n_queries, uint32_t query_planes,
+                           const ScanGeometry& geometry, uint64_t n, double* scores, uint64_t* ids,
+                           uint32_t* partitions, int64_t* accs, uint64_t* counts, SearchStats* stats = nullptr,
+                           ScanVariant variant = ScanVariant::Auto, uint32_t probe_tiles = 0) const;
     rbe_cuda_index* handle(size_t i) const { return handles_.at(i).get(); }
     size_t handle_count() const { return handles_.size(); }
 

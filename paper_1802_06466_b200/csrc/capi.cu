@@ -501,7 +501,8 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
         const size_t qbytes = size_t(n_queries) * query_planes * ix->shape.wpp * 8;
         ix->queries.ensure(qbytes);
         RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, ix->stream));
-        run_batch(ix, ix->stream, n_queries, query_planes, geometry, n, options, stats);
+        // without stats the batch runs with a single host synchronisation (after the D2H below)
+        run_batch(ix, ix->stream, n_queries, query_planes, geometry, n, options, stats, stats != nullptr);
         ix->ensure_host_out(size_t(n_queries) * n);
         RBE_CK(cudaMemcpyAsync(ix->host_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToHost,
                                ix->stream));

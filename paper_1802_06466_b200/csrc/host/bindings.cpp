@@ -231,48 +231,40 @@ PYBIND11_MODULE(_core, m) {
         .def(
             "search_words",
             [](const DeviceIndex& d, py::array_t<uint64_t, py::array::c_style | py::array::forcecast> words,
-               const ScanGeometry& g, uint64_t n, const std::string& variant, uint32_t probe_tiles) {
+               const ScanGeometry& g, uint64_t n, const std::string& variant, uint32_t probe_tiles, bool with_stats) {
                 if (words.ndim() != 3) throw std::invalid_argument("search_words: words must be [Q][planes][wpp]");
                 const uint32_t Q = uint32_t(words.shape(0)), qp = uint32_t(words.shape(1));
                 const ScanVariant v = parse_variant(variant);
-                SearchStats st;
-                std::vector<SelectionResult> res;
-                {
-                    py::gil_scoped_release nogil;
-                    res = d.search_words(std::span<const uint64_t>(words.data(), size_t(words.size())), Q, qp, g, n,
-                                         &st, v, probe_tiles);
-                }
+                // results land directly in the returned arrays (entries past counts[q] are zero)
                 py::array_t<double> scores({size_t(Q), size_t(n)});
                 py::array_t<uint64_t> ids({size_t(Q), size_t(n)});
                 py::array_t<uint32_t> parts({size_t(Q), size_t(n)});
                 py::array_t<int64_t> accs({size_t(Q), size_t(n)});
                 py::array_t<uint64_t> counts(Q);
-                auto S = scores.mutable_unchecked<2>();
-                auto I = ids.mutable_unchecked<2>();
-                auto P = parts.mutable_unchecked<2>();
-                auto A = accs.mutable_unchecked<2>();
-                auto C = counts.mutable_unchecked<1>();
-                for (uint32_t q = 0; q < Q; ++q) {
-                    const auto& e = res[q].entries;
-                    C(q) = e.size();
-                    for (uint64_t k = 0; k < n; ++k) {
-                        if (k < e.size()) {
-                            S(q, k) = e[k].score;
-                            I(q, k) = e[k].id;
-                            P(q, k) = e[k].partition;
-                            A(q, k) = e[k].acc;
-                        } else {
-                            S(q, k) = 0.0;
-                            I(q, k) = 0;
-                            P(q, k) = 0;
-                            A(q, k) = 0;
+                SearchStats st;
+                {
+                    double* S = scores.mutable_data();
+                    uint64_t* I = ids.mutable_data();
+                    uint32_t* P = parts.mutable_data();
+                    int64_t* A = accs.mutable_data();
+                    uint64_t* C = counts.mutable_data();
+                    py::gil_scoped_release nogil;
+                    d.search_words_into(std::span<const uint64_t>(words.data(), size_t(words.size())), Q, qp, g, n,
+                                        S, I, P, A, C, with_stats ? &st : nullptr, v, probe_tiles);
+                    for (uint32_t q = 0; q < Q; ++q) {
+                        const size_t o = size_t(q) * n;
+                        for (uint64_t k = C[q]; k < n; ++k) {
+                            S[o + k] = 0.0;
+                            I[o + k] = 0;
+                            P[o + k] = 0;
+                            A[o + k] = 0;
                         }
                     }
                 }
                 return py::make_tuple(scores, ids, parts, accs, counts, stats_dict(st));
             },
             py::arg("words"), py::arg("geometry"), py::arg("n"), py::arg("variant") = "auto",
-            py::arg("probe_tiles") = 0,
+            py::arg("probe_tiles") = 0, py::arg("with_stats") = true,
             "Batched search over raw query words [Q][planes][wpp] -> (scores, ids, partitions, accs, counts, stats)");
 
     // --- search (drop-in) and batch

@@ -456,6 +456,31 @@ std::vector<SelectionResult> DeviceIndex::search_words(std::span<const uint64_t>
     return out;
 }
 
+void DeviceIndex::search_words_into(std::span<const uint64_t> query_words, uint32_t n_queries, uint32_t query_planes,
+                                    const ScanGeometry& g, uint64_t n, double* scores, uint64_t* ids,
+                                    uint32_t* partitions, int64_t* accs, uint64_t* counts, SearchStats* stats,
+                                    ScanVariant variant, uint32_t probe_tiles) const {
+    const size_t wpp = PackedBinaryVector::words_for(dim_);
+    if (query_words.size() != size_t(n_queries) * query_planes * wpp)
+        throw std::invalid_argument("search: query buffer size does not match (Q, planes, dim)");
+    const rbe_scan_geometry geo{g.blocks, g.threads_per_block, g.items_per_thread, g.queue_length};
+    rbe_search_options opt{};
+    opt.variant = uint32_t(variant);
+    opt.probe_tiles = probe_tiles;
+    rbe_search_stats st{};
+    std::vector<rbe_cuda_index*> hs;
+    for (auto& h : handles_) hs.push_back(h.get());
+    ck(rbe_cuda_search_multi(hs.data(), uint32_t(hs.size()), query_words.data(), n_queries, query_planes, &geo, n,
+                             &opt, scores, ids, partitions, accs, counts, stats ? &st : nullptr));
+    if (stats) {
+        stats->scored += st.scored;
+        stats->variant = st.variant;
+        stats->candidates += st.candidates;
+        stats->survivors += st.survivors;
+        stats->device_ms += st.total_ms;
+    }
+}
+
 namespace {
 
 void check_query(const RbeEmbedding& q, uint32_t dim) {
