@@ -63,8 +63,11 @@ namespace {
 
 constexpr int kStages = 12;          // max ring depth (stages of sw docs)
 constexpr int kMaxWG = 3;            // worker warpgroups
-constexpr int kThreads = 416;        // 13 warps (roles: see tensor_scan_kernel), 128 registers each
-constexpr int kProducerWarp = 12;
+constexpr int kWGWarps = 4;          // warps per worker warpgroup (4: one per TMEM lane quadrant, 8: two)
+constexpr int kHalves = kWGWarps / 4;  // warps sharing each doc (split of its K blocks and queries)
+constexpr int kQH = 64 / kHalves;    // accumulator columns (queries) tested per warp
+constexpr int kThreads = 32 * (kMaxWG * kWGWarps + 1);  // workers + producer warp
+constexpr int kProducerWarp = kMaxWG * kWGWarps;
 constexpr uint32_t kCandQueue = 4096;  // deferred candidates per strip (shared memory; overflow is scored at once)
 constexpr int kAllBar = 8;           // named barrier of all worker threads
 constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
@@ -172,6 +175,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// a value the compiler cannot see through (keeps it from hoisting what is cheap to rebuild)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -228,6 +236,16 @@ __device__ __forceinline__ void tmem_ld32_p16(uint32_t taddr, uint32_t* v) {
           "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
           "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
           "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+// 32 columns, the low 16 bits of columns 2r and 2r+1 packed into register r
+__device__ __forceinline__ void tmem_ld16_p16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr)
         : "memory");
 }
@@ -474,6 +492,22 @@ __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, ui
     }
 }
 
+// A passing pair (F >= 0) of query q and the doc in slot i of logical thread y (mags_y):
+// recover acc exactly (F - X(j) = lambda (acc - C_q), j the magnitude bin the X block
+// used) and merge it (take_candidate).
+__device__ __noinline__ void take_pair(int32_t F, uint32_t q, uint32_t i, uint32_t col, const float* mags_y,
+                                       const int32_t* xc, int32_t cq, float m0f, float inv_df, uint32_t lam_shift,
+                                       unsigned int* error, uint32_t sw, const double* theta_s, uint32_t* st_key,
+                                       uint32_t tpb, int L, uint16_t* touched, uint32_t* tcount) {
+    const float mag = __ldg(mags_y + uint64_t(i) * tpb);
+    const uint32_t j = mag_bin(mag, m0f, inv_df);
+    const int32_t X = xc[q] - xc[kQPass + q] * int32_t(j) - xc[2 * kQPass + q] * int32_t(j >> 4);
+    const int32_t num = F - X;
+    if (num & ((1 << lam_shift) - 1)) atomicAdd(error, 1u);
+    const int32_t a = (num >> lam_shift) + cq;
+    take_candidate(a, q, mag, i, col, sw, theta_s, st_key, mags_y, tpb, L, touched, tcount);
+}
+
 // Warp roles (13 warps, 128 registers each):
 //   warps 0..4*nwg-1   workers: warpgroup w = warp/4 takes sub-tiles u = w (mod nwg)
 //                      (128 docs, CTA-local counter u); quadrant warp%4 = TMEM lanes.
@@ -491,14 +525,17 @@ __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, ui
 #define RBE_ACC(slot, v)
 #endif
 
-template <int KP, bool RW, bool PROBE>
+// W = 4: the common shape fixed at compile time -- dim 128 (w32 = 4), 256-doc strips, three
+// worker warpgroups (two in the probe); W = 0: every shape from TensorParams
+template <int KP, bool RW, bool PROBE, int W>
 __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const uint32_t w32 = p.w32;
+    constexpr bool kFixed = W == 4;
+    const uint32_t w32 = kFixed ? 4u : p.w32;
     const uint32_t nst = p.nstages;
-    const uint32_t nwg = p.nwg;                              // 2 or 3
-    const uint32_t n_workers = 128 * nwg;
-    const uint32_t sw = p.sw;                                // strip width (logical threads): 128 or 256
+    const uint32_t nwg = kFixed ? (PROBE ? 2u : 3u) : p.nwg;  // 2 or 3
+    const uint32_t n_workers = 32 * kWGWarps * nwg;
+    const uint32_t sw = kFixed ? 256u : p.sw;                // strip width (logical threads): 128 or 256
     const uint32_t spt = sw / 128;                           // 128-doc sub-tiles per stage
     const uint32_t spt_sh = spt == 2 ? 1 : 0;
     const uint32_t plane_bytes = sw * w32 * 4;               // one plane of a stage (sw docs)
@@ -518,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + sl.bars);
     uint64_t* full = bars;                // [nst]   stage loaded (tx bytes)
     uint64_t* empty = full + nst;         // [nst]   stage consumed (4 warp arrivals per sub-tile)
-    uint64_t* a_full = empty + nst;       // [kMaxWG] A complete and D free (4 warp arrivals)
+    uint64_t* a_full = empty + nst;       // [kMaxWG] (unused)
     uint64_t* mma_done = a_full + kMaxWG; // [kMaxWG] MMA committed
     uint64_t* x_ready = mma_done + kMaxWG;  // [2] X block of parity b rewritten (strip end)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_ready + 2);
@@ -564,10 +601,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < nst; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 4 * spt);
+            mbar_init(empty + s, kWGWarps * spt);
         }
         for (int w = 0; w < kMaxWG; ++w) {
-            mbar_init(a_full + w, 4);
             mbar_init(mma_done + w, 1);
         }
         mbar_init(x_ready + 0, 1);
@@ -609,25 +645,32 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 }
             }
         }
-    } else if (warp < int(4 * nwg)) {
+    } else if (warp < int(kWGWarps * nwg)) {
         // ===================== workers =====================
-        const uint32_t wg = uint32_t(warp >> 2);
+        // Warpgroup wg = warps [8 wg, 8 wg + 8).  Warp quadrant warp % 4 owns TMEM lanes
+        // (= docs of the sub-tile) [32 quad, 32 quad + 32); the two warps of a quadrant split
+        // each doc: half h expands data K blocks [h w32/2, (h+1) w32/2) (half 1 also the X
+        // block) and tests accumulator columns (queries) [32h, 32h + 32).
+        const uint32_t wg = uint32_t(warp) / kWGWarps;
+        const uint32_t half = kHalves == 2 ? (uint32_t(warp) >> 2) & 1u : 0u;
         const int quad = warp & 3;
         const uint32_t l = uint32_t(quad * 32 + lane);  // TMEM lane == doc within the sub-tile
         const uint32_t wt = uint32_t(threadIdx.x);      // worker thread id
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
+        const uint32_t hw = w32 / kHalves;              // data K blocks per half
+        const uint32_t qh = kQH * half;                 // first query (D column) of this half
         const uint32_t a_t0 = tmem_base + wg * wg_cols + lane_base;  // this warpgroup's A[0] (this warp's lanes)
-        const uint32_t d_t = tmem_base + wg * wg_cols + 2 * a_cols + lane_base;
+        const uint32_t d_t = a_t0 + 2 * a_cols + qh;
         const uint32_t pstride = p.ptop;
-        uint32_t scored = 0, cands = 0;
+        uint32_t cands = 0;
         uint32_t kc = 0;  // sub-tiles processed by this warpgroup (A buffer / barrier parities)
 #ifdef RBE_PHASE_PROF
         long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // registers: flushed once at the end
 #endif
-        float pm[PROBE ? kQPass : 1];
+        float pm[PROBE ? kQH : 1];
 #pragma unroll
-        for (int e = 0; e < (PROBE ? kQPass : 1); ++e) pm[e] = -INFINITY;
-        {
+        for (int e = 0; e < (PROBE ? kQH : 1); ++e) pm[e] = -INFINITY;
+        if (half == kHalves - 1) {
             // constant columns 2..7 of the X block of both A buffers (K bytes 8..31 = 255)
             uint32_t v[8] = {0u, 0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u};
             tmem_st8(a_t0 + 8 * w32, v);
@@ -635,64 +678,66 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             tmem_wait_st();
         }
 
-        // expand doc `col` of ring stage `st` into A buffer `ab`; returns its magnitude and bin
-        auto expand = [&](uint32_t st, uint32_t col, uint32_t ab, float& mag, uint32_t& j) {
+        // expand this half of doc `col` of ring stage `st` into A buffer `ab`; returns its magnitude
+        auto expand = [&](uint32_t st, uint32_t col, uint32_t ab, float& mag) {
             const uint8_t* stage = ring + st * stage_bytes;
             const uint32_t a_t = a_t0 + ab * a_cols;
-            if ((w32 & 3) == 0) {
-                // 16-byte loads: a warp reads 32 consecutive docs x 16 B = 512 B, conflict-free
-                const uint4* src = reinterpret_cast<const uint4*>(stage);
-                const uint32_t w128 = w32 / 4;
-                for (uint32_t g4 = 0; g4 < w128; ++g4) {
-                    uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
+            if constexpr (W == 4 && kHalves == 1) {
+                // one 16-byte load per plane: a warp reads 32 consecutive docs x 16 B, conflict-free
+                const uint4* src = reinterpret_cast<const uint4*>(stage) + col;
+                uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
 #pragma unroll
-                    for (int t = 0; t < KP; ++t) {
-                        const uint4 v = src[(t * sw + col) * w128 + g4];
-                        w0[t] = v.x;
-                        w1[t] = v.y;
-                        w2[t] = v.z;
-                        w3[t] = v.w;
-                    }
-                    uint32_t out[16];
-                    ExpandStored<KP, RW>::run(w0, out);
-                    ExpandStored<KP, RW>::run(w1, out + 8);
-                    tmem_st16(a_t + 32 * g4, out);
-                    ExpandStored<KP, RW>::run(w2, out);
-                    ExpandStored<KP, RW>::run(w3, out + 8);
-                    tmem_st16(a_t + 32 * g4 + 16, out);
+                for (int t = 0; t < KP; ++t) {
+                    const uint4 v = src[t * sw];
+                    w0[t] = v.x;
+                    w1[t] = v.y;
+                    w2[t] = v.z;
+                    w3[t] = v.w;
                 }
-            } else {
-                const uint2* src = reinterpret_cast<const uint2*>(stage);
-                const uint32_t w64 = w32 / 2;
-                for (uint32_t g2 = 0; g2 < w64; ++g2) {
-                    uint32_t w0[KP], w1[KP];
+                uint32_t out[16];
+                ExpandStored<KP, RW>::run(w0, out);
+                ExpandStored<KP, RW>::run(w1, out + 8);
+                tmem_st16(a_t, out);
+                ExpandStored<KP, RW>::run(w2, out);
+                ExpandStored<KP, RW>::run(w3, out + 8);
+                tmem_st16(a_t + 16, out);
+            } else if constexpr (W == 4) {
+                // two 8-byte words per plane: plane t, doc col, words [2h, 2h + 2)
+                const uint2* src = reinterpret_cast<const uint2*>(stage) + col * 2 + half;
+                uint32_t w0[KP], w1[KP];
 #pragma unroll
-                    for (int t = 0; t < KP; ++t) {
-                        const uint2 v = src[(t * sw + col) * w64 + g2];
-                        w0[t] = v.x;
-                        w1[t] = v.y;
-                    }
-                    uint32_t out[16];
+                for (int t = 0; t < KP; ++t) {
+                    const uint2 v = src[t * sw * 2];
+                    w0[t] = v.x;
+                    w1[t] = v.y;
+                }
+                uint32_t out[16];
+                ExpandStored<KP, RW>::run(w0, out);
+                ExpandStored<KP, RW>::run(w1, out + 8);
+                tmem_st16(a_t + 16 * half, out);
+            } else {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(stage) + col * w32 + hw * half;
+                for (uint32_t g = 0; g < hw; ++g) {
+                    uint32_t w0[KP];
+#pragma unroll
+                    for (int t = 0; t < KP; ++t) w0[t] = src[t * sw * w32 + g];
+                    uint32_t out[8];
                     ExpandStored<KP, RW>::run(w0, out);
-                    ExpandStored<KP, RW>::run(w1, out + 8);
-                    tmem_st16(a_t + 16 * g2, out);
+                    tmem_st8(a_t + 8 * (hw * half + g), out);
                 }
             }
             mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
-            j = mag_bin(mag, p.m0f, p.inv_df);
-            tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
+            if (half == kHalves - 1) {
+                const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
+                tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + st);  // this warp's share of the stage is consumed
         };
         // This warp's part of A(k) is complete and its reads of D are done.  The last of the
-        // warpgroup's four warps to get here issues MMA(k) (whole warp, one elected lane), so no
+        // warpgroup's eight warps to get here issues MMA(k) (whole warp, one elected lane), so no
         // warp ever waits for an issuer: the per-warpgroup counter in shared memory orders it.
-        const uint32_t idesc = idesc_i8(128, p.n_pad);
-        const uint64_t b_desc0 = smem_desc(smem_u32(bsm));
-        const uint64_t x_desc0 = smem_desc(smem_u32(xsm));
-        const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
-        const uint32_t a_w = tmem_base + wg * wg_cols;         // lane 0 of this warpgroup's A[0]
-        const uint32_t d_w = a_w + 2 * a_cols;
+        const uint32_t a_w = tmem_base + wg * wg_cols;  // lane 0 of this warpgroup's A[0]
         uint32_t xpar = 0;  // X block parity of the current strip
         auto arrive_a = [&](uint32_t ab) {
             tmem_wait_st();
@@ -705,10 +750,15 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                              : "r"(smem_u32(wg_arrivals + wg))
                              : "memory");
             old = __shfl_sync(0xffffffffu, old, 0);
-            if ((old & 3u) == 3u) {
+            if ((old & uint32_t(kWGWarps - 1)) == uint32_t(kWGWarps - 1)) {
                 tc_fence_after();
+                // descriptors rebuilt here (cheap, uniform) rather than held across the loop
+                const uint32_t idesc = idesc_i8(128, p.n_pad);
+                const uint64_t b_desc0 = smem_desc(opaque_u32(smem_u32(bsm)));
+                const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
+                const uint64_t xd = smem_desc(opaque_u32(smem_u32(xsm) + xpar * p.n_pad * 32));
                 const uint32_t a_t = a_w + ab * a_cols;
-                const uint64_t xd = x_desc0 + xpar * b_step;
+                const uint32_t d_w = a_w + 2 * a_cols;
                 switch (w32) {
                     case 2: mma_group<2>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
                     case 4: mma_group<4>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
@@ -722,29 +772,43 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
 
         uint32_t u0 = 0, tiles0 = 0, sidx = 0;
         for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x, ++sidx) {
-            const StripInfo si = strip_info(p, s);
-            const PartDesc& part = p.parts[si.part];
-            const uint32_t n_sub = si.n_tiles * spt;
-            const uint64_t lim = part.count > si.base ? part.count - si.base : 0;  // valid: i*tpb + col < lim
-            const int32_t* xc = xcoef + (sidx & 1) * 3 * kQPass;
-            const bool p16 = p16ok[sidx & 1] != 0;
+            // only what the sub-tile loop needs stays in registers; the strip's partition and base
+            // are recomputed (strip_info) where the rare candidate path and the strip end use them
+            uint32_t n_sub, n_tiles, lim;
+            {
+                const StripInfo si = strip_info(p, s);
+                const uint64_t count = p.parts[si.part].count;
+                n_tiles = si.n_tiles;
+                n_sub = n_tiles * spt;
+                // valid: i*tpb + col < lim (i*tpb < 2^31: tensor_supported)
+                const uint64_t lim64 = count > si.base ? count - si.base : 0;
+                lim = uint32_t(lim64 < 0xffffffffull ? lim64 : 0xffffffffull);
+                if (wt == 0 && !PROBE) {
+                    unsigned long long valid_docs = 0;
+                    for (uint32_t t = 0; t < n_tiles; ++t) {
+                        const uint64_t o = uint64_t(t) * p.tpb;
+                        valid_docs += o < lim64 ? (lim64 - o < sw ? lim64 - o : sw) : 0;
+                    }
+                    atomicAdd(p.scored, valid_docs * p.nq);
+                }
+            }
             xpar = sidx & 1;
             uint32_t k = (wg + nwg - u0 % nwg) % nwg;
             if (k < n_sub) {
+                // ring position of sub-tile k's stage; advanced incrementally (at most a few stages per step)
                 uint32_t ti = k >> spt_sh;
                 uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
                 auto seek = [&](uint32_t t_new) {
-                    for (; ti < t_new; ++ti)
-                        if (++st_idx == nst) {
-                            st_idx = 0;
-                            st_ph ^= 1;
-                        }
+                    st_idx += t_new - ti;
+                    ti = t_new;
+                    while (st_idx >= nst) {
+                        st_idx -= nst;
+                        st_ph ^= 1;
+                    }
                 };
                 float mag, mag_n = 0.0f;
-                uint32_t j, j_n = 0;
-                uint32_t col = (k & (spt - 1)) * 128 + l, col_n = 0;
                 mbar_wait(full + st_idx, st_ph);
-                expand(st_idx, col, kc & 1, mag, j);
+                expand(st_idx, (k & (spt - 1)) * 128 + l, kc & 1, mag);
                 arrive_a(kc & 1);
                 while (true) {
                     const uint32_t k_n = k + nwg;
@@ -753,15 +817,14 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     RBE_CLK(c0);
                     if (has_next) {
                         seek(k_n >> spt_sh);
-                        col_n = (k_n & (spt - 1)) * 128 + l;
                         mbar_wait(full + st_idx, st_ph);
                         RBE_CLK(c0b);
                         RBE_ACC(0, c0b - c0);
-                        expand(st_idx, col_n, (kc + 1) & 1, mag_n, j_n);
+                        expand(st_idx, (k_n & (spt - 1)) * 128 + l, (kc + 1) & 1, mag_n);
                     }
                     RBE_CLK(c1);
-                    const bool valid = uint64_t(i) * p.tpb + col < lim;
-                    scored += valid ? 1 : 0;
+                    const uint32_t col = (k & (spt - 1)) * 128 + l;
+                    const bool valid = i * p.tpb + col < lim;
                     mbar_wait_sleep(mma_done + wg, kc & 1);
                     tc_fence_after();
                     RBE_CLK(c2);
@@ -769,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         // F = lambda acc; per-thread maxima of the (float) score
                         const float scale = __fdiv_rn(ldexpf(1.0f, -L - int(p.lam_shift)), mag);
 #pragma unroll
-                        for (int c = 0; c < kQPass / 16; ++c) {
+                        for (int c = 0; c < kQH / 16; ++c) {
                             int32_t F[16];
                             tmem_ld16(d_t + 16 * c, F);
                             tmem_wait_ld();
@@ -781,69 +844,69 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         }
                     } else {
                         // F >= 0 is necessary for score >= theta: AND the sign bits per group of 8
-                        uint32_t gmask = 0;  // bit g: some F >= 0 among queries [8g, 8g+8)
-                        if (p16) {
-                            // low 16 bits of all 64 accumulators in 32 registers (pack::16b); the
+                        constexpr int kG = kQH / 8;  // groups of 8 queries per warp
+                        uint32_t gmask = 0;  // bit g: some F >= 0 among queries qh + [8g, 8g+8)
+                        if (p16ok[xpar] != 0) {
+                            // low 16 bits of the warp's accumulators, two per register (pack::16b); the
                             // sign of every F >= 0 survives, a wrapped F < 0 is rejected exactly below
-                            uint32_t R[32];
-                            tmem_ld32_p16(d_t, R);
+                            uint32_t R[kQH / 2];
+                            if constexpr (kQH == 64) tmem_ld32_p16(d_t, R);
+                            else tmem_ld16_p16(d_t, R);
                             tmem_wait_ld();
-                            uint32_t a4[4];
+                            uint32_t a4[kG];
 #pragma unroll
-                            for (int g = 0; g < 4; ++g) {
-                                uint32_t a = R[8 * g];
+                            for (int g = 0; g < kG; ++g) a4[g] = (R[4 * g] & R[4 * g + 1]) & (R[4 * g + 2] & R[4 * g + 3]);
+                            uint32_t all = a4[0];
 #pragma unroll
-                                for (int e2 = 1; e2 < 8; ++e2) a &= R[8 * g + e2];
-                                a4[g] = a;
-                            }
-                            const uint32_t all = (a4[0] & a4[1]) & (a4[2] & a4[3]);
+                            for (int g = 1; g < kG; ++g) all &= a4[g];
                             if ((~all & 0x80008000u) && valid) {
 #pragma unroll
-                                for (int g = 0; g < kQPass / 8; ++g) {
-                                    const uint32_t a = (R[4 * g] & R[4 * g + 1]) & (R[4 * g + 2] & R[4 * g + 3]);
-                                    gmask |= uint32_t((~a & 0x80008000u) != 0u) << g;
-                                }
+                                for (int g = 0; g < kG; ++g) gmask |= uint32_t((~a4[g] & 0x80008000u) != 0u) << g;
                             }
                         } else {
-                            int32_t F[kQPass];
-                            tmem_ld32(d_t, F);
-                            tmem_ld32(d_t + 32, F + 32);
-                            tmem_wait_ld();
 #pragma unroll
-                            for (int g = 0; g < kQPass / 8; ++g) {
-                                uint32_t a = uint32_t(F[8 * g]);
+                            for (int c = 0; c < kQH / 16; ++c) {
+                                int32_t F[16];
+                                tmem_ld16(d_t + 16 * c, F);
+                                tmem_wait_ld();
 #pragma unroll
-                                for (int e2 = 1; e2 < 8; ++e2) a &= uint32_t(F[8 * g + e2]);
-                                gmask |= (~a >> 31) << g;
+                                for (int g = 0; g < 2; ++g) {
+                                    uint32_t a = uint32_t(F[8 * g]);
+#pragma unroll
+                                    for (int e2 = 1; e2 < 8; ++e2) a &= uint32_t(F[8 * g + e2]);
+                                    gmask |= (~a >> 31) << (2 * c + g);
+                                }
                             }
                             if (!valid) gmask = 0;
                         }
                         // groups with a passing pair in any lane (tcgen05.ld is warp-collective)
                         uint32_t wmask = __reduce_or_sync(0xffffffffu, gmask);
-                        while (wmask) {
-                            const uint32_t g = uint32_t(__ffs(wmask) - 1);
-                            wmask &= wmask - 1;
-                            int32_t v[8];
-                            tmem_ld8(d_t + 8 * g, v);
-                            tmem_wait_ld();
-                            if (!((gmask >> g) & 1)) continue;
+                        if (wmask) {
+                            do {
+                                const uint32_t g = uint32_t(__ffs(wmask) - 1);
+                                wmask &= wmask - 1;
+                                int32_t v[8];
+                                tmem_ld8(d_t + 8 * g, v);
+                                tmem_wait_ld();
+                                if (!((gmask >> g) & 1)) continue;
 #pragma unroll
-                            for (int e2 = 0; e2 < 8; ++e2) {
-                                if (v[e2] < 0) continue;
-                                ++cands;
-                                const uint32_t q = 8 * g + uint32_t(e2);
-                                const int32_t X = xc[q] - xc[kQPass + q] * int32_t(j) - xc[2 * kQPass + q] * int32_t(j >> 4);
-                                const int32_t num = v[e2] - X;
-                                if (num & ((1 << p.lam_shift) - 1)) atomicAdd(p.error, 1u);
-                                const int32_t a = (num >> p.lam_shift) + cq_s[q];
-                                // defer to the strip end (exact FP64 scoring in bulk); score now if full
-                                const uint32_t pos = atomicAdd(cq_count, 1u);
-                                if (pos < kCandQueue)
-                                    cqueue[pos] = make_uint2((q << 26) | i, (col << 24) | (uint32_t(a) & 0xffffffu));
-                                else
-                                    take_candidate(a, q, mag, i, col, sw, theta_s, st_key, part.mags + si.base + col,
-                                                   p.tpb, L, touched, tcount);
-                            }
+                                for (int e2 = 0; e2 < 8; ++e2) {
+                                    if (v[e2] < 0) continue;
+                                    ++cands;
+                                    const uint32_t q = qh + 8 * g + uint32_t(e2);
+                                    // defer to the strip end (acc recovery + exact FP64 scoring in bulk;
+                                    // 0 <= F < 2^24); score now if the queue is full
+                                    const uint32_t pos = atomicAdd(cq_count, 1u);
+                                    if (pos < kCandQueue)
+                                        cqueue[pos] = make_uint2((q << 26) | i, (col << 24) | uint32_t(v[e2]));
+                                    else {
+                                        const StripInfo si = strip_info(p, s);
+                                        take_pair(v[e2], q, i, col, p.parts[si.part].mags + si.base + col,
+                                                  xcoef + xpar * 3 * kQPass, cq_s[q], p.m0f, p.inv_df, p.lam_shift,
+                                                  p.error, sw, theta_s, st_key, p.tpb, L, touched, tcount);
+                                    }
+                                }
+                            } while (wmask);
                         }
                     }
                     ++kc;
@@ -855,15 +918,15 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     if (!has_next) break;
                     arrive_a(kc & 1);  // A(k+nwg) ready (kc already advanced), D read
                     k = k_n;
-                    col = col_n;
                     mag = mag_n;
-                    j = j_n;
                 }
                 tc_fence_before();
             }
             u0 += n_sub;
-            tiles0 += si.n_tiles;
+            tiles0 += n_tiles;
             RBE_CLK(c4);
+            const StripInfo si = strip_info(p, s);
+            const PartDesc& part = p.parts[si.part];
             // ================= strip end (all worker threads) =================
             if (PROBE) {
                 // merge the warpgroups' per-lane maxima: the lanes of warpgroup w always hold
@@ -873,8 +936,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 for (uint32_t w = 0; w < nwg; ++w) {
                     if (w == wg) {
 #pragma unroll
-                        for (int e = 0; e < kQPass; ++e) {
-                            float* m = pmax + e * sw + colp;
+                        for (int e = 0; e < kQH; ++e) {
+                            float* m = pmax + (qh + e) * sw + colp;
                             *m = fmaxf(*m, pm[e]);
                             pm[e] = -INFINITY;
                         }
@@ -883,7 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 }
                 // per query keep the top ptop per-thread maxima of the strip (distinct threads)
                 const uint32_t vpl = sw / 32;
-                for (uint32_t q = uint32_t(warp); q < p.nq; q += 4 * nwg) {
+                for (uint32_t q = uint32_t(warp); q < p.nq; q += kWGWarps * nwg) {
                     float v[8];
 #pragma unroll
                     for (int k2 = 0; k2 < 8; ++k2) v[k2] = uint32_t(k2) < vpl ? pmax[q * sw + 32 * k2 + lane] : -INFINITY;
@@ -918,10 +981,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 for (uint32_t k2 = wt; k2 < nc; k2 += n_workers) {
                     const uint2 c = cqueue[k2];
                     const uint32_t q = c.x >> 26, ii = c.x & 0x3ffffffu, cc = c.y >> 24;
-                    const int32_t a = int32_t(c.y << 8) >> 8;
-                    const float mg = __ldg(part.mags + si.base + cc + uint64_t(ii) * p.tpb);
-                    take_candidate(a, q, mg, ii, cc, sw, theta_s, st_key, part.mags + si.base + cc, p.tpb, L, touched,
-                                   tcount);
+                    take_pair(int32_t(c.y & 0xffffffu), q, ii, cc, part.mags + si.base + cc,
+                              xcoef + (sidx & 1) * 3 * kQPass, cq_s[q], p.m0f, p.inv_df, p.lam_shift, p.error, sw,
+                              theta_s, st_key, p.tpb, L, touched, tcount);
                 }
             }
             named_bar(kAllBar, n_workers);
@@ -1041,15 +1103,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             for (int k2 = 0; k2 < 8; ++k2) p.prof[uint64_t(blockIdx.x) * 8 + k2] += prof_acc[k2];
 #endif
         if (!PROBE) {
-            unsigned long long sc64 = (unsigned long long)scored * p.nq, cd64 = cands;
-            for (int off = 16; off > 0; off >>= 1) {
-                sc64 += __shfl_xor_sync(0xffffffffu, sc64, off);
-                cd64 += __shfl_xor_sync(0xffffffffu, cd64, off);
-            }
-            if (lane == 0) {
-                atomicAdd(p.scored, sc64);
-                atomicAdd(p.candidates, cd64);
-            }
+            unsigned long long cd64 = cands;
+            for (int off = 16; off > 0; off >>= 1) cd64 += __shfl_xor_sync(0xffffffffu, cd64, off);
+            if (lane == 0 && cd64) atomicAdd(p.candidates, cd64);
         }
     }
     tc_fence_before();
@@ -1202,7 +1258,8 @@ uint64_t count_strips(const rbe_scan_geometry& g, uint64_t count) {
 
 template <int KP, bool RW, bool PROBE>
 void launch_kernel(const TensorParams& tp, size_t smem, int grid, cudaStream_t st) {
-    auto k = tensor_scan_kernel<KP, RW, PROBE>;
+    const bool fixed = tp.w32 == 4 && tp.sw == 256 && tp.nwg == (PROBE ? 2u : 3u);
+    auto k = fixed ? tensor_scan_kernel<KP, RW, PROBE, 4> : tensor_scan_kernel<KP, RW, PROBE, 0>;
     RBE_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k<<<grid, kThreads, smem, st>>>(tp);
     RBE_CK(cudaGetLastError());
@@ -1296,6 +1353,7 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
     if (pick_stages(s.kp, s.w32, strip_width(g)) == 0) return no("shared memory");
     if (pick_lam_shift(s, qp) < 0) return no("accumulator range exceeds the threshold block");
     if (g.items_per_thread >= 511) return no("items_per_thread >= 511 (state key)");
+    if (uint64_t(g.items_per_thread) * g.threads_per_block >= (1ull << 31)) return no("logical block span >= 2^31 slots");
     {
         const uint64_t rqmax = s.rw ? ((1ull << qp) - 1) : qp, vmax = s.rw ? ((1ull << s.kp) - 1) : s.kp;
         if (64ull * s.wpp * rqmax * vmax >= (1ull << 22)) return no("accumulator range exceeds the state key");
