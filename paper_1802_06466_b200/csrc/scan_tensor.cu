@@ -72,6 +72,7 @@ constexpr uint32_t kCandQueue = 4096;  // deferred candidates per strip (shared 
 constexpr int kAllBar = 8;           // named barrier of all worker threads
 constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
 constexpr uint32_t kEmptyKey = ~0u;      // state key: (i << 23) | (acc & 0x7fffff), i < 511, |acc| < 2^22
+constexpr uint32_t kThetaCap = 32768;  // probe values per query theta_kernel reads
 constexpr int kBins = 64;            // dynamic-theta histogram bins per query
 constexpr int kHiCols = 24;          // X block: K bytes 8..31 hold 255 (the c_q "high" part)
 constexpr int32_t kXMax = 255 * kHiCols * 127 + 127;  // largest |X| the block can encode
@@ -447,8 +448,8 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uin
     off = al(off + size_t(n_pad) * 32 * w32);
     s.xb = off;  // two X blocks (threshold), indexed by strip parity
     off = al(off + 2 * size_t(n_pad) * 32);
-    s.state = off;
-    off = al(off + size_t(kQPass) * sw * 4);
+    s.state = off;  // probe: two [64][sw] float buffers (strip parity)
+    off = al(off + size_t(kQPass) * sw * 4 * (probe ? 2 : 1));
     s.cqueue = off;  // also the strip end's histogram / counters scratch
     off = al(off + (probe ? 0 : size_t(kCandQueue) * 8));
     s.touched = off;
@@ -933,7 +934,19 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 // logical threads (w % spt) * 128 + l when nwg is a multiple of spt; otherwise
                 // (spt == 2, nwg == 3) the probe runs with one column per warpgroup (host)
                 const uint32_t colp = (wg % spt) * 128 + l;
-                for (uint32_t w = 0; w < nwg; ++w) {
+                const bool owned = nwg == spt;  // every column is held by exactly one warpgroup
+                float* pmx = owned ? pmax + (sidx & 1) * kQPass * sw : pmax;  // double-buffered by strip parity
+                if (owned) {
+                    // owners store (no merge, no reset: every column is rewritten each strip); the
+                    // other parity's buffer is still being read by warps selecting the previous strip
+#pragma unroll
+                    for (int e = 0; e < kQH; ++e) {
+                        pmx[(qh + e) * sw + colp] = pm[e];
+                        pm[e] = -INFINITY;
+                    }
+                    named_bar(kAllBar, n_workers);
+                }
+                for (uint32_t w = 0; w < (owned ? 0u : nwg); ++w) {
                     if (w == wg) {
 #pragma unroll
                         for (int e = 0; e < kQH; ++e) {
@@ -944,34 +957,24 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     }
                     named_bar(kAllBar, n_workers);
                 }
-                // per query keep the top ptop per-thread maxima of the strip (distinct threads)
+                // per query, ptop (32 or 16) maxima of disjoint groups of the strip's per-thread
+                // maxima (lane-wise over the lane's sw/32 columns, then lane pairs): the n-th largest
+                // of maxima over disjoint groups of distinct threads still bounds the final n-th
+                // survivor from below (theta_kernel), and no warp-serial selection is needed
                 const uint32_t vpl = sw / 32;
                 for (uint32_t q = uint32_t(warp); q < p.nq; q += kWGWarps * nwg) {
-                    float v[8];
+                    float mx = -INFINITY;
 #pragma unroll
-                    for (int k2 = 0; k2 < 8; ++k2) v[k2] = uint32_t(k2) < vpl ? pmax[q * sw + 32 * k2 + lane] : -INFINITY;
-                    for (uint32_t r = 0; r < pstride; ++r) {
-                        float best = v[0];
-#pragma unroll
-                        for (int k2 = 1; k2 < 8; ++k2) best = fmaxf(best, v[k2]);
-                        float mx = best;
-                        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-                        const unsigned holder = __ballot_sync(0xffffffffu, best == mx);
-                        if (lane == __ffs(holder) - 1) {
-                            bool done = false;
-#pragma unroll
-                            for (int k2 = 0; k2 < 8; ++k2)
-                                if (!done && v[k2] == mx) {
-                                    v[k2] = -INFINITY;
-                                    done = true;
-                                }
-                        }
-                        if (lane == 0) p.probe_out[(uint64_t(p.q0 + q) * p.n_strips + s) * pstride + r] = mx;
-                    }
+                    for (int k2 = 0; k2 < 8; ++k2)
+                        if (uint32_t(k2) < vpl) mx = fmaxf(mx, pmx[q * sw + 32 * k2 + lane]);
+                    if (pstride == 16) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                    if (lane < pstride) p.probe_out[(uint64_t(p.q0 + q) * p.n_strips + s) * pstride + lane] = mx;
                 }
-                named_bar(kAllBar, n_workers);
-                for (uint32_t k2 = wt; k2 < kQPass * sw; k2 += n_workers) pmax[k2] = -INFINITY;
-                named_bar(kAllBar, n_workers);
+                if (!owned) {
+                    named_bar(kAllBar, n_workers);
+                    for (uint32_t k2 = wt; k2 < kQPass * sw; k2 += n_workers) pmax[k2] = -INFINITY;
+                    named_bar(kAllBar, n_workers);
+                }
                 continue;
             }
             named_bar(kAllBar, n_workers);
@@ -1160,7 +1163,6 @@ __global__ void prepare_queries_tensor_kernel(const uint64_t* __restrict__ q, ui
 }
 
 // ------------------------------------------------------------ threshold
-constexpr uint32_t kThetaCap = 32768;
 
 // theta_q = (n-th largest probe value) lowered by a relative 2^-16 margin
 // (probe scores are FP32 approximations with relative error < 2^-20), or -inf
@@ -1298,7 +1300,9 @@ uint32_t pick_nwg(uint32_t w32) {
 // ring depth: as many stages (<= kStages) as shared memory allows
 uint32_t pick_stages(uint32_t kp, uint32_t w32, uint32_t sw) {
     for (uint32_t ns = kStages; ns >= 2; --ns)
-        if (smem_layout(kp, w32, kQPass, ns, sw, false).total <= kSmemLimit) return ns;
+        if (smem_layout(kp, w32, kQPass, ns, sw, false).total <= kSmemLimit &&
+            smem_layout(kp, w32, kQPass, ns, sw, true).total <= kSmemLimit)
+            return ns;
     return 0;
 }
 
@@ -1379,9 +1383,9 @@ TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geom
     pl.n_strips = pl.prefix.back();
     const uint32_t passes = (Q + kQPass - 1) / kQPass;
     pl.query_bytes = size_t(passes) * kQPass * 64 * s.wpp + size_t(Q) * 4 + 256;
-    // probe values per (query, strip): enough that n of them exist when the probe covers
-    // the corpus thinly (a few strips), at least 4
-    pl.ptop = uint32_t(std::min<uint64_t>(32, std::max<uint64_t>(4, pl.n_strips ? (2 * n + pl.n_strips - 1) / pl.n_strips : 4)));
+    // probe values per (query, strip): 32 lane maxima while all strips' fit theta_kernel's
+    // window, else 16 lane-pair maxima
+    pl.ptop = pl.n_strips * 32 <= kThetaCap ? 32u : 16u;  // group maxima per (query, strip)
     pl.probe_bytes = size_t(Q) * pl.n_strips * pl.ptop * sizeof(float) + 256;
     pl.threshold_bytes = size_t(Q) * (32 + kBins * 4) + 64;
     pl.state_bytes = sizeof(uint64_t) * pl.prefix.size() + 64;

@@ -1,8 +1,9 @@
 #!/bin/bash
-# Run under gpurun: one `ncu --set full` capture of the main tensor scan launch only
-# (the probe launch is -s 1 skipped), tag $1.
+# Run under gpurun: one `ncu --set full` capture of one tensor scan launch, tag $1;
+# $2 = launches to skip (1: the main scan after the probe, 0: the probe).
 TAG=${1:-dev}
+SKIP=${2:-1}
 ncu --set full --clock-control none --import-source on \
-    -k regex:tensor_scan_kernel -s 1 -c 1 -o gpurun_out/prof_$TAG -f \
+    -k regex:tensor_scan_kernel -s $SKIP -c 1 -o gpurun_out/prof_$TAG -f \
     timeout -s KILL 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/prof_$TAG.log 2>&1
 echo "ncu rc=$?"
