@@ -632,17 +632,23 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             RingPos rs;
             for (uint64_t s = blockIdx.x; s < p.n_strips; s += gridDim.x) {
                 const StripInfo si = strip_info(p, s);
-                const PartDesc& part = p.parts[si.part];
+                // the partition descriptor in registers (a reference would be re-read from global
+                // memory after every bulk copy's memory clobber, serialising the ring on L2 latency)
+                const PartDesc part = p.parts[si.part];
+                const uint64_t plane_words = part.count_pad * w32;       // u32 words between planes
+                const uint32_t* src = part.planes + si.base * w32;       // plane 0 of tile 0
+                const float* msrc = part.mags + si.base;
+                const uint64_t tile_words = uint64_t(p.tpb) * w32;
                 for (uint32_t i = 0; i < si.n_tiles; ++i, rs.next(nst)) {
                     mbar_wait_sleep(empty + rs.idx, rs.phase ^ 1);
                     mbar_expect_tx(full + rs.idx, stage_bytes);
-                    const uint64_t slot0 = si.base + uint64_t(i) * p.tpb;
                     uint8_t* dst = ring + rs.idx * stage_bytes;
 #pragma unroll
                     for (int t = 0; t < KP; ++t)
-                        bulk_g2s(dst + t * plane_bytes, part.planes + (uint64_t(t) * part.count_pad + slot0) * w32,
-                                 plane_bytes, full + rs.idx);
-                    bulk_g2s(dst + KP * plane_bytes, part.mags + slot0, sw * 4, full + rs.idx);
+                        bulk_g2s(dst + t * plane_bytes, src + t * plane_words, plane_bytes, full + rs.idx);
+                    bulk_g2s(dst + KP * plane_bytes, msrc, sw * 4, full + rs.idx);
+                    src += tile_words;
+                    msrc += p.tpb;
                 }
             }
         }
@@ -917,7 +923,10 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     RBE_ACC(3, c3 - c2);
                     RBE_ACC(5, 1);
                     if (!has_next) break;
+                    RBE_CLK(c6);
                     arrive_a(kc & 1);  // A(k+nwg) ready (kc already advanced), D read
+                    RBE_CLK(c7);
+                    RBE_ACC(6, c7 - c6);
                     k = k_n;
                     mag = mag_n;
                 }
@@ -1102,8 +1111,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             RBE_ACC(4, c5 - c4);
         }
 #ifdef RBE_PHASE_PROF
-        if (p.prof && lane == 0 && warp == 1)
-            for (int k2 = 0; k2 < 8; ++k2) p.prof[uint64_t(blockIdx.x) * 8 + k2] += prof_acc[k2];
+        if (p.prof && lane == 0)  // per worker warp: [grid][16][8]
+            for (int k2 = 0; k2 < 8; ++k2) p.prof[(uint64_t(blockIdx.x) * 16 + warp) * 8 + k2] += prof_acc[k2];
 #endif
         if (!PROBE) {
             unsigned long long cd64 = cands;
@@ -1471,7 +1480,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     const int grid = int(std::min<uint64_t>(n_strips, uint64_t(sm_count())));
     static unsigned long long* d_prof = nullptr;
     const bool prof = getenv("RBE_PROF") != nullptr;
-    if (prof && !d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 2048 * 8));
+    if (prof && !d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 2048 * 16 * 8));
     for (uint32_t ps = 0; ps < passes; ++ps) {
         tp.q0 = ps * kQPass;
         tp.nq = std::min<uint32_t>(kQPass, Q - tp.q0);
@@ -1492,21 +1501,24 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
         // main pass
         tp.probe_tiles = 0;
         if (prof) {
-            RBE_CK(cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * 2048 * 8, st));
+            RBE_CK(cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * 2048 * 16 * 8, st));
             tp.prof = d_prof;
         }
         dispatch<false>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, false).total, grid, st);
         tp.prof = nullptr;
         if (prof) {
-            std::vector<unsigned long long> h(size_t(grid) * 8);
+            std::vector<unsigned long long> h(size_t(grid) * 16 * 8);
             RBE_CK(cudaMemcpyAsync(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost, st));
             RBE_CK(cudaStreamSynchronize(st));
-            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int b = 0; b < grid; ++b)
-                for (int k = 0; k < 8; ++k) acc[k] += double(h[size_t(b) * 8 + k]);
-            fprintf(stderr, "[rbe prof] worker warp per sub-tile: wait full %.0f, expand(+wait) %.0f, wait MMA %.0f, test %.0f; "
-                            "strip ends %.0f per CTA (n=%.0f)\n",
-                    acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[4] / grid, acc[5]);
+            for (int w = 0; w < 4 * int(tp.nwg); ++w) {
+                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int b = 0; b < grid; ++b)
+                    for (int k = 0; k < 8; ++k) acc[k] += double(h[(size_t(b) * 16 + w) * 8 + k]);
+                fprintf(stderr, "[rbe prof] warp %2d per sub-tile: wait full %.0f, expand %.0f, wait MMA %.0f, test %.0f, "
+                                "arrive+issue %.0f; strip ends %.0f per CTA (n=%.0f)\n",
+                        w, acc[0] / acc[5], acc[1] / acc[5], acc[2] / acc[5], acc[3] / acc[5], acc[6] / acc[5],
+                        acc[4] / grid, acc[5]);
+            }
         }
         launches += 3;
     }
