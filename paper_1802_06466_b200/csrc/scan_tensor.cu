@@ -62,13 +62,20 @@ namespace rbe_dev {
 namespace {
 
 constexpr int kStages = 12;          // max ring depth (stages of sw docs)
-constexpr int kMaxWG = 3;            // worker warpgroups
+constexpr int kMaxWG = 4;            // worker warpgroups
+// The X (threshold) K block of the doc operand lives in shared memory, not TMEM: TMEM then
+// holds per warpgroup two data A operands (8 w32 columns each) and one accumulator, four
+// warpgroups at dim 128.  X tile of (warpgroup, A buffer): 128 rows x 16 B (K bytes 0..15,
+// core matrices packed, SBO 128); K bytes 16..31 (all 255) come from one shared constant
+// tile reached through the descriptor's leading byte offset.
+constexpr uint32_t kXTile = 128 * 16;
 constexpr int kWGWarps = 4;          // warps per worker warpgroup (4: one per TMEM lane quadrant, 8: two)
 constexpr int kHalves = kWGWarps / 4;  // warps sharing each doc (split of its K blocks and queries)
 constexpr int kQH = 64 / kHalves;    // accumulator columns (queries) tested per warp
 constexpr int kThreads = 32 * (kMaxWG * kWGWarps + 1);  // workers + producer warp
 constexpr int kProducerWarp = kMaxWG * kWGWarps;
-constexpr uint32_t kCandQueue = 4096;  // deferred candidates per strip (shared memory; overflow is scored at once)
+constexpr uint32_t kCandQueue = 2560;  // deferred candidates per strip (shared memory; overflow is scored at once)
+constexpr uint32_t kTouchedCap = 4096;  // state entries listed per strip (beyond: the strip end scans the table)
 constexpr int kAllBar = 8;           // named barrier of all worker threads
 constexpr int kQPass = 64;           // queries per pass (= MMA N; state is [64][128] in shared memory)
 constexpr uint32_t kEmptyKey = ~0u;      // state key: (i << 23) | (acc & 0x7fffff), i < 511, |acc| < 2^22
@@ -288,12 +295,24 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
         : "memory");
 }
 // one sub-tile: NKB data K blocks + the X block, accumulating into d
+// A and B from shared memory (the X block)
+__device__ __forceinline__ void mma_i8_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// one sub-tile: NKB data K blocks (A in TMEM) + the X block (A in shared memory), into d
 template <int NKB>
-__device__ __forceinline__ void mma_group(uint32_t d, uint32_t a, uint64_t b0, uint64_t b_step, uint64_t xd,
-                                          uint32_t idesc) {
+__device__ __forceinline__ void mma_group(uint32_t d, uint32_t a, uint64_t b0, uint64_t b_step, uint64_t ax,
+                                          uint64_t xd, uint32_t idesc) {
 #pragma unroll
     for (int kb = 0; kb < NKB; ++kb) mma_i8_elect(d, a + 8 * kb, b0 + kb * b_step, idesc, kb > 0);
-    mma_i8_elect(d, a + 8 * NKB, xd, idesc, 1);
+    mma_i8_ss_elect(d, ax, xd, idesc, 1);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -315,6 +334,16 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
     d |= uint64_t(256 >> 4) << 32;  // stride byte offset
     d |= uint64_t(1) << 46;         // descriptor version (Blackwell)
     return d;                       // base offset 0, layout SWIZZLE_NONE
+}
+
+// same with explicit leading / stride byte offsets
+__device__ __forceinline__ uint64_t smem_desc_lbo(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3fffu);
+    d |= uint64_t((lbo >> 4) & 0x3fffu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3fffu) << 32;
+    d |= uint64_t(1) << 46;
+    return d;
 }
 
 // instruction descriptor: D s32, A u8 (doc V bytes), B s8 (query 2*rq), K-major both
@@ -432,7 +461,7 @@ struct RingPos {
 };
 
 struct SmemLayout {
-    size_t b, xb, state, cqueue, touched, qconst, bars, total;
+    size_t b, xb, state, cqueue, touched, qconst, bars, ax, total;
 };
 
 __host__ __device__ inline size_t stage_bytes_of(uint32_t kp, uint32_t w32, uint32_t sw) {
@@ -451,13 +480,16 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uin
     s.state = off;  // probe: two [64][sw] float buffers (strip parity)
     off = al(off + size_t(kQPass) * sw * 4 * (probe ? 2 : 1));
     s.cqueue = off;  // also the strip end's histogram / counters scratch
-    off = al(off + (probe ? 0 : size_t(kCandQueue) * 8));
+    // (the strip end's counters and histogram, 17 KB, reuse it)
+    off = al(off + (probe ? 0 : std::max<size_t>(size_t(kCandQueue) * 8, kQPass * (4 + 8 + 4 * kBins))));
     s.touched = off;
-    off = al(off + (probe ? 0 : size_t(kQPass) * sw * 2));
+    off = al(off + (probe ? 0 : size_t(kTouchedCap) * 2));
     s.qconst = off;
     off = al(off + kQPass * 8 + kQPass * 4 + 2 * 3 * kQPass * 4 + 16);
     s.bars = off;
     off = al(off + (2 * nstages + 2 * kMaxWG + 2) * 8 + 64);
+    s.ax = off;  // [kMaxWG][2] X tiles + the constant tile
+    off = al(off + (2 * kMaxWG + 1) * size_t(kXTile));
     s.total = off;
     return s;
 }
@@ -486,7 +518,10 @@ __device__ __noinline__ void take_candidate(int32_t a, uint32_t q, float mag, ui
         }
         const uint32_t prev = atomicCAS(ent, cur, mine);
         if (prev == cur) {
-            if (cur == kEmptyKey) touched[atomicAdd(tcount, 1u)] = uint16_t(q * sw + col);  // first entry
+            if (cur == kEmptyKey) {  // first entry
+                const uint32_t pos = atomicAdd(tcount, 1u);
+                if (pos < kTouchedCap) touched[pos] = uint16_t(q * sw + col);
+            }
             break;
         }
         cur = prev;
@@ -534,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     constexpr bool kFixed = W == 4;
     const uint32_t w32 = kFixed ? 4u : p.w32;
     const uint32_t nst = p.nstages;
-    const uint32_t nwg = kFixed ? (PROBE ? 2u : 3u) : p.nwg;  // 2 or 3
+    const uint32_t nwg = kFixed ? (PROBE ? 2u : 4u) : p.nwg;  // 2..4
     const uint32_t n_workers = 32 * kWGWarps * nwg;
     const uint32_t sw = kFixed ? 256u : p.sw;                // strip width (logical threads): 128 or 256
     const uint32_t spt = sw / 128;                           // 128-doc sub-tiles per stage
@@ -566,7 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t a_cols = 8 * (w32 + 1);  // TMEM columns of one A (4 K bytes per column)
+    const uint32_t a_cols = 8 * w32;        // TMEM columns of one A (data K blocks, 4 K bytes per column)
+    uint8_t* axs = smem + sl.ax;            // X tiles of the doc operand
     const uint32_t d_cols = p.n_pad;        // TMEM columns of one D
     const uint32_t wg_cols = 2 * a_cols + d_cols;
     uint32_t tmem_cols = 32;
@@ -591,6 +627,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             write_xrow(xsm + b * p.n_pad * 32, p.n_pad, 0, q, x);
         }
     }
+    for (uint32_t e = threadIdx.x; e < kXTile / 4; e += blockDim.x)  // constant X tile: K bytes 16..31 = 255
+        reinterpret_cast<uint32_t*>(smem + sl.ax + 2 * kMaxWG * kXTile)[e] = ~0u;
     if (threadIdx.x < 2) p16ok[threadIdx.x] = 1u;
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < p.nq; q += blockDim.x)
@@ -677,12 +715,11 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
         float pm[PROBE ? kQH : 1];
 #pragma unroll
         for (int e = 0; e < (PROBE ? kQH : 1); ++e) pm[e] = -INFINITY;
+        // this thread's row (doc l) in its warpgroup's two X tiles: bytes 0..7 per doc, 8..15 = 255
+        uint8_t* ax_row = axs + (wg * 2) * kXTile + (l / 8) * 128 + (l % 8) * 16;
         if (half == kHalves - 1) {
-            // constant columns 2..7 of the X block of both A buffers (K bytes 8..31 = 255)
-            uint32_t v[8] = {0u, 0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u};
-            tmem_st8(a_t0 + 8 * w32, v);
-            tmem_st8(a_t0 + a_cols + 8 * w32, v);
-            tmem_wait_st();
+            *reinterpret_cast<uint2*>(ax_row + 8) = make_uint2(~0u, ~0u);
+            *reinterpret_cast<uint2*>(ax_row + kXTile + 8) = make_uint2(~0u, ~0u);
         }
 
         // expand this half of doc `col` of ring stage `st` into A buffer `ab`; returns its magnitude
@@ -736,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
             if (half == kHalves - 1) {
                 const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
-                tmem_st2(a_t + 8 * w32, j * 0x01010101u, (j >> 4) | 0x100u);
+                *reinterpret_cast<uint2*>(ax_row + ab * kXTile) = make_uint2(j * 0x01010101u, (j >> 4) | 0x100u);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + st);  // this warp's share of the stage is consumed
@@ -748,6 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
         uint32_t xpar = 0;  // X block parity of the current strip
         auto arrive_a = [&](uint32_t ab) {
             tmem_wait_st();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the X row, for the tensor core
             tc_fence_before();
             __syncwarp();
             uint32_t old = 0;
@@ -766,11 +804,13 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 const uint64_t xd = smem_desc(opaque_u32(smem_u32(xsm) + xpar * p.n_pad * 32));
                 const uint32_t a_t = a_w + ab * a_cols;
                 const uint32_t d_w = a_w + 2 * a_cols;
+                const uint32_t ax_addr = opaque_u32(smem_u32(axs)) + (wg * 2 + ab) * kXTile;
+                const uint64_t ax_desc = smem_desc_lbo(ax_addr, (2 * kMaxWG - (wg * 2 + ab)) * kXTile, 128);
                 switch (w32) {
-                    case 2: mma_group<2>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
-                    case 4: mma_group<4>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
-                    case 6: mma_group<6>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
-                    default: mma_group<8>(d_w, a_t, b_desc0, b_step, xd, idesc); break;
+                    case 2: mma_group<2>(d_w, a_t, b_desc0, b_step, ax_desc, xd, idesc); break;
+                    case 4: mma_group<4>(d_w, a_t, b_desc0, b_step, ax_desc, xd, idesc); break;
+                    case 6: mma_group<6>(d_w, a_t, b_desc0, b_step, ax_desc, xd, idesc); break;
+                    default: mma_group<8>(d_w, a_t, b_desc0, b_step, ax_desc, xd, idesc); break;
                 }
                 mma_commit_elect(mma_done + wg);
                 __syncwarp();
@@ -1007,7 +1047,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 uint32_t* scnt = reinterpret_cast<uint32_t*>(cqueue);                             // [64]
                 unsigned long long* sbase = reinterpret_cast<unsigned long long*>(scnt + kQPass);  // [64]
                 uint32_t* hist_s = reinterpret_cast<uint32_t*>(sbase + kQPass);                    // [64][kBins]
-                const uint32_t nt = *tcount;
+                // entries to visit: the touched list, or the whole table when it overflowed
+                const bool scan_all = *tcount > kTouchedCap;
+                const uint32_t nt = scan_all ? kQPass * sw : *tcount;
                 if (wt < kQPass) scnt[wt] = 0;
                 for (uint32_t k2 = wt; k2 < kQPass * kBins; k2 += n_workers) hist_s[k2] = 0;
                 named_bar(kAllBar, n_workers);
@@ -1021,11 +1063,13 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     return sc >= theta_s[q];  // theta may have risen since the entry was set
                 };
                 for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
+                    const uint32_t ent = scan_all ? k2 : touched[k2];
+                    if (scan_all && st_key[ent] == kEmptyKey) continue;
                     uint32_t q;
                     uint64_t slot;
                     int32_t a;
                     double sc;
-                    if (survivor(touched[k2], q, slot, a, sc)) atomicAdd(scnt + q, 1u);
+                    if (survivor(ent, q, slot, a, sc)) atomicAdd(scnt + q, 1u);
                 }
                 named_bar(kAllBar, n_workers);
                 if (wt < p.nq) {
@@ -1034,7 +1078,8 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 }
                 named_bar(kAllBar, n_workers);
                 for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
-                    const uint32_t ent = touched[k2];
+                    const uint32_t ent = scan_all ? k2 : touched[k2];
+                    if (scan_all && st_key[ent] == kEmptyKey) continue;
                     uint32_t q;
                     uint64_t slot;
                     int32_t a;
@@ -1269,7 +1314,7 @@ uint64_t count_strips(const rbe_scan_geometry& g, uint64_t count) {
 
 template <int KP, bool RW, bool PROBE>
 void launch_kernel(const TensorParams& tp, size_t smem, int grid, cudaStream_t st) {
-    const bool fixed = tp.w32 == 4 && tp.sw == 256 && tp.nwg == (PROBE ? 2u : 3u);
+    const bool fixed = tp.w32 == 4 && tp.sw == 256 && tp.nwg == (PROBE ? 2u : 4u);
     auto k = fixed ? tensor_scan_kernel<KP, RW, PROBE, 4> : tensor_scan_kernel<KP, RW, PROBE, 0>;
     RBE_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k<<<grid, kThreads, smem, st>>>(tp);
@@ -1299,10 +1344,10 @@ void dispatch(uint32_t kp, bool rw, const TensorParams& tp, size_t smem, int gri
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-// TMEM: per warpgroup two A operands (K = 32 (w32 + 1) bytes) and one 64-column accumulator
+// TMEM: per warpgroup two A operands (data K = 32 w32 bytes) and one 64-column accumulator
 uint32_t pick_nwg(uint32_t w32) {
     for (uint32_t n = kMaxWG; n >= 2; --n)
-        if (n * (2 * 8 * (w32 + 1) + kQPass) <= 512) return n;
+        if (n * (2 * 8 * w32 + kQPass) <= 512) return n;
     return 0;
 }
 

@@ -234,3 +234,18 @@ def test_tensor_matches_reference(rbe, port, case):
     assert stats["scored"] == scored == Q * N
     assert got == want, case
     check_accs(got, accs, mags_by_id(parts), qp, kp, rw)
+
+
+def test_tensor_state_table_overflow(rbe, port):
+    """n above the survivor count (theta stays -inf): every (query, logical thread)
+    state entry of a strip is set -- 40 queries x 256 threads > the 4096-entry
+    touched list, so the strip end scans the whole table.  Tensor == reference."""
+    N, dim, kp, qp, geo, n, Q = 40000, 128, 3, 3, (1, 256, 256, 1), 60000, 40
+    ref = Ref()
+    parts = synthetic_partitions(17, N, dim, kp, 1, True, port)
+    qs = gen_queries(19, Q, dim, qp)
+    want, scored = ref.index(dim, kp, True, parts).search(qs, geo, n)
+    dix = device_index(rbe, dim, kp, True, parts)
+    got, accs, counts, stats = gpu_search(rbe, dix, qs, geo, n, "tensor")
+    assert stats["variant"] == "tensor"
+    assert got == want
