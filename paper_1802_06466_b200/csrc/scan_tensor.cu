@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 const float* msrc = part.mags + si.base;
                 const uint64_t tile_words = uint64_t(p.tpb) * w32;
                 for (uint32_t i = 0; i < si.n_tiles; ++i, rs.next(nst)) {
-                    mbar_wait_sleep(empty + rs.idx, rs.phase ^ 1);
+                    mbar_wait(empty + rs.idx, rs.phase ^ 1);
                     mbar_expect_tx(full + rs.idx, stage_bytes);
                     uint8_t* dst = ring + rs.idx * stage_bytes;
 #pragma unroll
