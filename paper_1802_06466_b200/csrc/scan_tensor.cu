@@ -40,15 +40,18 @@
 // per-thread best of a distinct logical thread), and the X block of the
 // query operand is rewritten in shared memory.
 //
-// Kernel anatomy (one CTA per SM, persistent over 128-doc "strips" = the
-// 128 logical threads y in [128h, 128h+128) of logical block x):
-//   warp 4*nwg    producer: cp.async.bulk of each sub-tile's plane words and
+// Kernel anatomy (one CTA per SM, persistent over "strips" = the sw (256 or
+// 128) logical threads [hs*sw, hs*sw + sw) of a logical block; a strip's tile i
+// is sw contiguous slots, split into sw/128 sub-tiles of 128 docs):
+//   warp 16       producer: cp.async.bulk of each tile's plane words and
 //                 magnitudes into a shared-memory ring (mbarrier complete_tx);
 //                 TMEM allocator
-//   warpgroups    nwg (2..4) workers; warpgroup w takes sub-tiles u = w (mod
-//                 nwg): expand bit planes -> u8 V bytes -> tcgen05.st into its
-//                 A; its leader issues the MMAs (A from TMEM, B = queries from
-//                 shared memory) into its D; the warpgroup then tests D.
+//   warpgroups    nwg (2..4, four at dim 128) workers; warpgroup w takes
+//                 sub-tiles u = w (mod nwg): expand bit planes -> u8 V bytes ->
+//                 tcgen05.st into its A (data K blocks; the X block row goes to
+//                 shared memory); the last of its four warps to arrive issues the
+//                 MMAs into its D (A from TMEM / shared memory, B = queries from
+//                 shared memory); the warpgroup then tests D.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -544,14 +547,14 @@ __device__ __noinline__ void take_pair(int32_t F, uint32_t q, uint32_t i, uint32
     take_candidate(a, q, mag, i, col, sw, theta_s, st_key, mags_y, tpb, L, touched, tcount);
 }
 
-// Warp roles (13 warps, 128 registers each):
+// Warp roles (17 warps, 120 registers each):
 //   warps 0..4*nwg-1   workers: warpgroup w = warp/4 takes sub-tiles u = w (mod nwg)
 //                      (128 docs, CTA-local counter u); quadrant warp%4 = TMEM lanes.
 //                      Per warpgroup, software-pipelined within a strip:
 //                        expand(k+1) -> A[(k+1)&1] while the tensor core runs MMA(k);
 //                        wait MMA(k); test D; the last warp of the four to finish issues
 //                        MMA(k+1) (A(k+1) ready, D free)
-//   warp 12            producer: one contiguous sw-doc stage per tile; TMEM allocator
+//   warp 16            producer: one contiguous sw-doc stage per tile; TMEM allocator
 // phase timing of the worker loop (build with RBE_NVCC_EXTRA=-DRBE_PHASE_PROF, run with RBE_PROF=1)
 #ifdef RBE_PHASE_PROF
 #define RBE_CLK(x) const long long x = clock64()
