@@ -170,6 +170,29 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
             : "memory");
     } while (!ok);
 }
+// waits expected to be long-ish (the tensor core's queue): poll, then nap between polls so a
+// waiting warp issues a few instructions instead of waking on every barrier event in the CTA
+__device__ __forceinline__ void mbar_wait_nap(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    while (!ok) {
+        __nanosleep(64);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
 // long waits (the producer on a full ring): back off so the spinning warp does
 // not steal issue slots from the working ones
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
@@ -875,7 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     RBE_CLK(c1);
                     const uint32_t col = (k & (spt - 1)) * 128 + l;
                     const bool valid = i * p.tpb + col < lim;
-                    mbar_wait_sleep(mma_done + wg, kc & 1);
+                    mbar_wait_nap(mma_done + wg, kc & 1);
                     tc_fence_after();
                     RBE_CLK(c2);
                     if (PROBE) {
