@@ -17,7 +17,7 @@ namespace {
 
 constexpr int kThreads = 1024;
 constexpr uint32_t kCap = 8192;    // keys sorted in shared memory
-constexpr uint32_t kSmall = 2048;  // direct sort / radix-select stop size (bitonic cost grows as m log^2 m)
+constexpr uint32_t kSmall = 1024;  // direct sort / radix-select stop size: one key per thread (reg_bitonic)
 
 struct Key {
     uint64_t hi, lo;
@@ -66,6 +66,55 @@ __device__ void smem_bitonic(uint64_t* kh, uint64_t* kl, uint32_t* ix, uint32_t 
             __syncthreads();
         }
     }
+}
+
+// Bitonic sort of kh/kl/ix[0, n) ascending (n <= blockDim.x = 1024), one key per thread:
+// partner exchanges at distance j < 32 by warp shuffles, larger ones through shared
+// memory; the keys beyond n sort last (padded with ~0).  Result written back to kh/kl/ix.
+__device__ void reg_bitonic(uint64_t* kh, uint64_t* kl, uint32_t* ix, uint32_t n) {
+    const uint32_t t = threadIdx.x;
+    uint64_t h = ~0ull, lo = ~0ull;
+    uint32_t x = 0xffffffffu;
+    if (t < n) {
+        h = kh[t];
+        lo = kl[t];
+        x = ix[t];
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= kThreads; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            uint64_t ph, pl;
+            uint32_t px;
+            if (j >= 32) {
+                kh[t] = h;
+                kl[t] = lo;
+                ix[t] = x;
+                __syncthreads();
+                ph = kh[t ^ j];
+                pl = kl[t ^ j];
+                px = ix[t ^ j];
+                __syncthreads();
+            } else {
+                ph = __shfl_xor_sync(0xffffffffu, h, j);
+                pl = __shfl_xor_sync(0xffffffffu, lo, j);
+                px = __shfl_xor_sync(0xffffffffu, x, j);
+            }
+            const bool asc = (t & k) == 0;
+            const bool lower = (t & j) == 0;
+            const bool p_less = key_less(ph, pl, h, lo);
+            // the lower slot keeps the smaller key when ascending, the larger otherwise
+            const bool take = lower == asc ? p_less : !p_less && (ph != h || pl != lo);
+            if (take) {
+                h = ph;
+                lo = pl;
+                x = px;
+            }
+        }
+    }
+    kh[t] = h;
+    kl[t] = lo;
+    ix[t] = x;
+    __syncthreads();
 }
 
 __device__ void global_bitonic(const Result* in, uint32_t* ix, uint32_t n, uint32_t n2) {
@@ -122,18 +171,12 @@ __global__ void __launch_bounds__(kThreads) select_topn_kernel(const Result* __r
     if (n_eff == 0) return;
 
     if (m <= kSmall) {
-        uint32_t n2 = 1;
-        while (n2 < m) n2 <<= 1;
-        for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
-            if (i < m) {
-                const Key k = key_of(in[i]);
-                kh[i] = k.hi; kl[i] = k.lo; ix[i] = i;
-            } else {
-                kh[i] = ~0ull; kl[i] = ~0ull; ix[i] = 0xffffffffu;
-            }
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const Key k = key_of(in[i]);
+            kh[i] = k.hi; kl[i] = k.lo; ix[i] = i;
         }
         __syncthreads();
-        smem_bitonic(kh, kl, ix, n2);
+        reg_bitonic(kh, kl, ix, uint32_t(m));
         for (uint64_t k = threadIdx.x; k < n_eff; k += blockDim.x) out[k] = in[ix[k]];
         return;
     }
@@ -192,16 +235,28 @@ __global__ void __launch_bounds__(kThreads) select_topn_kernel(const Result* __r
     }
     __syncthreads();
     const uint32_t nb = s_bcnt;
-    uint32_t n2 = 1;
-    while (n2 < nb) n2 <<= 1;
-    for (uint32_t i = nb + threadIdx.x; i < n2; i += blockDim.x) { kh[i] = ~0ull; kl[i] = ~0ull; ix[i] = 0xffffffffu; }
-    __syncthreads();
-    smem_bitonic(kh, kl, ix, n2);
+    if (nb <= kThreads) {
+        reg_bitonic(kh, kl, ix, nb);
+    } else {
+        uint32_t n2 = 1;
+        while (n2 < nb) n2 <<= 1;
+        for (uint32_t i = nb + threadIdx.x; i < n2; i += blockDim.x) { kh[i] = ~0ull; kl[i] = ~0ull; ix[i] = 0xffffffffu; }
+        __syncthreads();
+        smem_bitonic(kh, kl, ix, n2);
+    }
     const uint32_t below = s_cnt;
     for (uint32_t k = threadIdx.x; k < r; k += blockDim.x) sel[below + k] = ix[k];
     __syncthreads();
     // ---- sort the n_eff selected entries
-    if (n_eff <= kCap) {
+    if (n_eff <= kThreads) {
+        for (uint32_t i = threadIdx.x; i < n_eff; i += blockDim.x) {
+            const Key k = key_of(in[sel[i]]);
+            kh[i] = k.hi; kl[i] = k.lo; ix[i] = sel[i];
+        }
+        __syncthreads();
+        reg_bitonic(kh, kl, ix, uint32_t(n_eff));
+        for (uint64_t k = threadIdx.x; k < n_eff; k += blockDim.x) out[k] = in[ix[k]];
+    } else if (n_eff <= kCap) {
         uint32_t n3 = 1;
         while (n3 < n_eff) n3 <<= 1;
         for (uint32_t i = threadIdx.x; i < n3; i += blockDim.x) {
