@@ -32,11 +32,11 @@ __device__ __forceinline__ void group(uint32_t d, uint32_t a, uint64_t b0, uint6
         : "memory");
 }
 
-__global__ void __launch_bounds__(32, 1) k(int iters, int inflight, unsigned long long* out) {
-    __shared__ __align__(1024) uint8_t bsm[5 * 64 * 32];
+__global__ void __launch_bounds__(32, 1) k(int iters, int inflight, unsigned long long* out, int N) {
+    __shared__ __align__(1024) uint8_t bsm[5 * 256 * 32];
     __shared__ uint32_t slot;
     __shared__ __align__(8) uint64_t bars[8];
-    for (int i = threadIdx.x; i < 5 * 64 * 32; i += 32) bsm[i] = 1;
+    for (int i = threadIdx.x; i < 5 * 256 * 32; i += 32) bsm[i] = 1;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     if (threadIdx.x < 8) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[threadIdx.x])));
@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(32, 1) k(int iters, int inflight, unsigned lon
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t idesc = (2u << 4) | (1u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
-    const uint64_t b0 = smem_desc(smem_u32(bsm)), step = (64 * 32) >> 4;
+    const uint32_t idesc = (2u << 4) | (1u << 10) | ((uint32_t(N) >> 3) << 17) | ((128u >> 4) << 24);
+    const uint64_t b0 = smem_desc(smem_u32(bsm)), step = (N * 32) >> 4;
     const long long t0 = clock64();
     uint32_t ph[4] = {0, 0, 0, 0};
     for (int it = 0; it < iters; ++it) {
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(32, 1) k(int iters, int inflight, unsigned lon
             ph[s] ^= 1;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
-        group(slot + 160 + 64 * s, slot + 40 * s, b0, step, idesc, &bars[s]);
+        group(slot + 160 + (N == 64 ? 64 * s : 0), slot + 40 * s, b0, step, idesc, &bars[s]);
     }
     for (int s = 0; s < inflight && s < iters; ++s) {
         while (!mtry(&bars[s], ph[s])) {
@@ -76,15 +76,16 @@ int main() {
     unsigned long long* d;
     cudaMalloc(&d, 8 * 1024);
     unsigned long long h[1024];
-    for (int inflight = 1; inflight <= 4; ++inflight) {
+    for (int N : {64, 128, 256})
+    for (int inflight = 1; inflight <= (N == 64 ? 4 : 1); ++inflight) {
         const int iters = 2000;
-        k<<<sms, 32>>>(iters, inflight, d);
+        k<<<sms, 32>>>(iters, inflight, d, N);
         if (cudaDeviceSynchronize() != cudaSuccess) { printf("err %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
         cudaMemcpy(h, d, 8 * sms, cudaMemcpyDeviceToHost);
         double m = 0;
         for (int i = 0; i < sms; ++i) m += h[i];
         m /= sms;
-        printf("groups in flight %d: %.0f cycles per 5-MMA group (M128 N64 K32 i8, A in TMEM)\n", inflight, m / iters);
+        printf("N=%d groups in flight %d: %.0f cycles per 5-MMA group (M128 K32 i8, A in TMEM)\n", N, inflight, m / iters);
     }
     return 0;
 }
