@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     constexpr bool kFixed = W == 4;
     const uint32_t w32 = kFixed ? 4u : p.w32;
     const uint32_t nst = p.nstages;
-    const uint32_t nwg = kFixed ? (PROBE ? 2u : 4u) : p.nwg;  // 2..4
+    const uint32_t nwg = kFixed ? 4u : p.nwg;  // 2..4
     const uint32_t n_workers = 32 * kWGWarps * nwg;
     const uint32_t sw = kFixed ? 256u : p.sw;                // strip width (logical threads): 128 or 256
     const uint32_t spt = sw / 128;                           // 128-doc sub-tiles per stage
@@ -1009,15 +1009,29 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 // logical threads (w % spt) * 128 + l when nwg is a multiple of spt; otherwise
                 // (spt == 2, nwg == 3) the probe runs with one column per warpgroup (host)
                 const uint32_t colp = (wg % spt) * 128 + l;
-                const bool owned = nwg == spt;  // every column is held by exactly one warpgroup
+                // every column is held by exactly one warpgroup (nwg == spt) or by two (nwg == 2 spt:
+                // warpgroups w and w + spt)
+                const bool owned = nwg == spt || nwg == 2 * spt;
                 float* pmx = owned ? pmax + (sidx & 1) * kQPass * sw : pmax;  // double-buffered by strip parity
                 if (owned) {
-                    // owners store (no merge, no reset: every column is rewritten each strip); the
-                    // other parity's buffer is still being read by warps selecting the previous strip
+                    // the first holder stores (no reset: every column is rewritten each strip), the
+                    // second folds its maxima in; the other parity's buffer is still being read by
+                    // warps selecting the previous strip
+                    if (wg < spt) {
 #pragma unroll
-                    for (int e = 0; e < kQH; ++e) {
-                        pmx[(qh + e) * sw + colp] = pm[e];
-                        pm[e] = -INFINITY;
+                        for (int e = 0; e < kQH; ++e) {
+                            pmx[(qh + e) * sw + colp] = pm[e];
+                            pm[e] = -INFINITY;
+                        }
+                    }
+                    named_bar(kAllBar, n_workers);
+                    if (wg >= spt) {
+#pragma unroll
+                        for (int e = 0; e < kQH; ++e) {
+                            float* m = pmx + (qh + e) * sw + colp;
+                            *m = fmaxf(*m, pm[e]);
+                            pm[e] = -INFINITY;
+                        }
                     }
                     named_bar(kAllBar, n_workers);
                 }
@@ -1340,7 +1354,7 @@ uint64_t count_strips(const rbe_scan_geometry& g, uint64_t count) {
 
 template <int KP, bool RW, bool PROBE>
 void launch_kernel(const TensorParams& tp, size_t smem, int grid, cudaStream_t st) {
-    const bool fixed = tp.w32 == 4 && tp.sw == 256 && tp.nwg == (PROBE ? 2u : 4u);
+    const bool fixed = tp.w32 == 4 && tp.sw == 256 && tp.nwg == 4u;
     auto k = fixed ? tensor_scan_kernel<KP, RW, PROBE, 4> : tensor_scan_kernel<KP, RW, PROBE, 0>;
     RBE_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k<<<grid, kThreads, smem, st>>>(tp);
@@ -1561,7 +1575,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
         {
             // probe: a warpgroup's lanes must always hold the same logical threads (nwg = spt)
             TensorParams pp = tp;
-            if (tp.sw > 128) pp.nwg = 2;
+            if (tp.sw > 128 && tp.nwg % 2) pp.nwg = 2;  // nwg a multiple of spt (4 stays)
             dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
         }
         const size_t tsm = size_t(kThetaCap) * 4;
