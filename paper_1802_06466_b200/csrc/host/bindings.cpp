@@ -231,16 +231,42 @@ PYBIND11_MODULE(_core, m) {
         .def(
             "search_words",
             [](const DeviceIndex& d, py::array_t<uint64_t, py::array::c_style | py::array::forcecast> words,
-               const ScanGeometry& g, uint64_t n, const std::string& variant, uint32_t probe_tiles, bool with_stats) {
+               const ScanGeometry& g, uint64_t n, const std::string& variant, uint32_t probe_tiles, bool with_stats,
+               py::object out) {
                 if (words.ndim() != 3) throw std::invalid_argument("search_words: words must be [Q][planes][wpp]");
                 const uint32_t Q = uint32_t(words.shape(0)), qp = uint32_t(words.shape(1));
                 const ScanVariant v = parse_variant(variant);
-                // results land directly in the returned arrays (entries past counts[q] are zero)
-                py::array_t<double> scores({size_t(Q), size_t(n)});
-                py::array_t<uint64_t> ids({size_t(Q), size_t(n)});
-                py::array_t<uint32_t> parts({size_t(Q), size_t(n)});
-                py::array_t<int64_t> accs({size_t(Q), size_t(n)});
-                py::array_t<uint64_t> counts(Q);
+                // results land directly in the returned arrays (entries past counts[q] are zero); with
+                // out=(scores, ids, partitions, accs, counts) the caller's arrays are reused (a serving
+                // loop then writes warm pages instead of faulting in fresh ones every batch)
+                using F = py::array;
+                py::array_t<double, F::c_style> scores;
+                py::array_t<uint64_t, F::c_style> ids;
+                py::array_t<uint32_t, F::c_style> parts;
+                py::array_t<int64_t, F::c_style> accs;
+                py::array_t<uint64_t, F::c_style> counts;
+                if (out.is_none()) {
+                    scores = py::array_t<double, F::c_style>({size_t(Q), size_t(n)});
+                    ids = py::array_t<uint64_t, F::c_style>({size_t(Q), size_t(n)});
+                    parts = py::array_t<uint32_t, F::c_style>({size_t(Q), size_t(n)});
+                    accs = py::array_t<int64_t, F::c_style>({size_t(Q), size_t(n)});
+                    counts = py::array_t<uint64_t, F::c_style>(Q);
+                } else {
+                    py::tuple t = out.cast<py::tuple>();
+                    if (t.size() != 5) throw std::invalid_argument("search_words: out must be (scores, ids, partitions, accs, counts)");
+                    auto take = [&](auto& dst, size_t k, size_t want) {
+                        using A = std::decay_t<decltype(dst)>;
+                        if (!A::check_(t[k])) throw std::invalid_argument("search_words: out array has the wrong dtype or layout");
+                        dst = t[k].cast<A>();
+                        if (size_t(dst.size()) != want || !dst.writeable())
+                            throw std::invalid_argument("search_words: out array has the wrong size or is read-only");
+                    };
+                    take(scores, 0, size_t(Q) * n);
+                    take(ids, 1, size_t(Q) * n);
+                    take(parts, 2, size_t(Q) * n);
+                    take(accs, 3, size_t(Q) * n);
+                    take(counts, 4, size_t(Q));
+                }
                 SearchStats st;
                 {
                     double* S = scores.mutable_data();
@@ -264,7 +290,7 @@ PYBIND11_MODULE(_core, m) {
                 return py::make_tuple(scores, ids, parts, accs, counts, stats_dict(st));
             },
             py::arg("words"), py::arg("geometry"), py::arg("n"), py::arg("variant") = "auto",
-            py::arg("probe_tiles") = 0, py::arg("with_stats") = true,
+            py::arg("probe_tiles") = 0, py::arg("with_stats") = true, py::arg("out") = py::none(),
             "Batched search over raw query words [Q][planes][wpp] -> (scores, ids, partitions, accs, counts, stats)");
 
     // --- search (drop-in) and batch

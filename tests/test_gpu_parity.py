@@ -249,3 +249,25 @@ def test_tensor_state_table_overflow(rbe, port):
     got, accs, counts, stats = gpu_search(rbe, dix, qs, geo, n, "tensor")
     assert stats["variant"] == "tensor"
     assert got == want
+
+
+def test_search_words_out_buffers(rbe, port):
+    """search_words(out=...) writes into the caller's arrays (reused across batches) and
+    returns them; results equal the freshly allocated ones."""
+    N, dim, kp, qp, geo, n = 20000, 128, 3, 3, (1, 256, 256, 1), 200
+    parts = synthetic_partitions(23, N, dim, kp, 1, True, port)
+    dix = device_index(rbe, dim, kp, True, parts)
+    qs = gen_queries(29, 5, dim, qp)
+    g = geometry(rbe, geo)
+    want = dix.search_words(qs, g, n, "auto")
+    out = (np.full((5, n), 7.0), np.zeros((5, n), np.uint64), np.zeros((5, n), np.uint32),
+           np.zeros((5, n), np.int64), np.zeros(5, np.uint64))
+    for _ in range(2):
+        got = dix.search_words(qs, g, n, "auto", 0, False, out)
+        for a, b, o in zip(got[:5], want[:5], out):
+            assert a is o
+            assert np.array_equal(a, b)
+    with pytest.raises(ValueError):
+        dix.search_words(qs, g, n, "auto", 0, False, out[:4])
+    with pytest.raises(ValueError):
+        dix.search_words(qs, g, n, "auto", 0, False, (out[0].astype(np.float32),) + out[1:])
