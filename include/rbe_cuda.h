@@ -159,6 +159,12 @@ int rbe_cuda_search_device(rbe_cuda_index* index, const uint64_t* d_query_words,
  * batch (CUDA events on the batch's stream); waits for that batch. */
 int rbe_cuda_index_last_batch_ms(rbe_cuda_index* index, double* scan_ms, double* total_ms);
 
+/* Page-locked host buffers (cudaMallocHost).  rbe_cuda_search detects output buffers in
+ * page-locked memory and copies the results straight into them (DMA, no host-side
+ * staging); pageable buffers work too, through a staging copy. */
+int rbe_cuda_host_alloc(size_t bytes, void** out);
+int rbe_cuda_host_free(void* ptr);
+
 /* Merge `n_lists` result lists per query (d_in = rbe_result[n_lists][n_queries][n],
  * device memory on `device`) into the top n per query under (score desc,
  * id asc): d_out = rbe_result[n_queries][n]. */

@@ -25,3 +25,24 @@ from ._lib._core import *  # noqa: F401,F403,E402
 
 LIB_DIR = _LIB
 CUDA_LIBRARY = _os.path.join(_LIB, "librbe_cuda.so")
+
+
+def pinned_empty(shape, dtype=float):
+    """numpy array in page-locked host memory (rbe_cuda_host_alloc).  Used as the ``out=``
+    arrays of ``DeviceIndex.search_words``, results are DMA'd straight into it."""
+    import ctypes
+    import weakref
+
+    import numpy as np
+
+    lib = ctypes.CDLL(CUDA_LIBRARY)
+    dt = np.dtype(dtype)
+    count = int(np.prod(shape)) if not isinstance(shape, int) else shape
+    nbytes = max(count * dt.itemsize, 1)
+    ptr = ctypes.c_void_p()
+    if lib.rbe_cuda_host_alloc(ctypes.c_size_t(nbytes), ctypes.byref(ptr)) != 0:
+        lib.rbe_cuda_last_error.restype = ctypes.c_char_p
+        raise RuntimeError(lib.rbe_cuda_last_error().decode())
+    buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, lib.rbe_cuda_host_free, ctypes.c_void_p(ptr.value))
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)

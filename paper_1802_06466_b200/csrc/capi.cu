@@ -106,7 +106,7 @@ struct rbe_cuda_index {
     cudaEvent_t ev[4] = {};
     std::mutex mu;
     // per-batch scratch, grown on demand
-    DevBuf queries, qperm, qtensor, surv, surv_count, counters, queue_scratch, sel_scratch, out, probe, thresholds;
+    DevBuf queries, qperm, qtensor, surv, surv_count, counters, queue_scratch, sel_scratch, out, probe, thresholds, soa;
     bool mag_range_ok = false;   // cached magnitude range (tensor threshold bins)
     float mag_lo = 0.0f, mag_hi = 0.0f;
     Result* host_out = nullptr;  // pinned staging for the D2H of results
@@ -123,7 +123,7 @@ struct rbe_cuda_index {
     ~rbe_cuda_index() {
         cudaSetDevice(device);
         for (DevBuf* b : {&queries, &qperm, &qtensor, &surv, &surv_count, &counters, &queue_scratch, &sel_scratch, &out,
-                          &probe, &thresholds})
+                          &probe, &thresholds, &soa})
             b->release();
         if (d_parts) cudaFree(d_parts);
         if (store) cudaFree(store);
@@ -135,6 +135,17 @@ struct rbe_cuda_index {
 };
 
 namespace {
+
+// true if p points into page-locked host memory (cudaMallocHost / cudaHostRegister)
+bool pinned_host(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
 
 void check_device_usable(int device) {
     int n = 0;
@@ -503,7 +514,29 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
         RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, ix->stream));
         // without stats the batch runs with a single host synchronisation (after the D2H below)
         run_batch(ix, ix->stream, n_queries, query_planes, geometry, n, options, stats, stats != nullptr);
-        ix->ensure_host_out(size_t(n_queries) * n);
+        const size_t ne = size_t(n_queries) * n;
+        if (pinned_host(scores) && pinned_host(ids) && pinned_host(partitions) && pinned_host(counts) &&
+            (!accs || pinned_host(accs))) {
+            // caller buffers in pinned host memory: convert to their layout on the device and DMA
+            // straight into them (no staging, no host scatter)
+            const size_t b8 = ne * 8, b4 = ne * 4;
+            ix->soa.ensure(3 * b8 + b4 + size_t(n_queries) * 8 + 256);
+            uint8_t* base = static_cast<uint8_t*>(ix->soa.p);
+            double* dS = reinterpret_cast<double*>(base);
+            uint64_t* dI = reinterpret_cast<uint64_t*>(base + b8);
+            int64_t* dA = reinterpret_cast<int64_t*>(base + 2 * b8);
+            uint64_t* dC = reinterpret_cast<uint64_t*>(base + 3 * b8);
+            uint32_t* dP = reinterpret_cast<uint32_t*>(base + 3 * b8 + size_t(n_queries) * 8);
+            launch_results_to_soa(ix->out.as<Result>(), n_queries, n, dS, dI, dP, accs ? dA : nullptr, dC, ix->stream);
+            RBE_CK(cudaMemcpyAsync(scores, dS, b8, cudaMemcpyDeviceToHost, ix->stream));
+            RBE_CK(cudaMemcpyAsync(ids, dI, b8, cudaMemcpyDeviceToHost, ix->stream));
+            RBE_CK(cudaMemcpyAsync(partitions, dP, b4, cudaMemcpyDeviceToHost, ix->stream));
+            if (accs) RBE_CK(cudaMemcpyAsync(accs, dA, b8, cudaMemcpyDeviceToHost, ix->stream));
+            RBE_CK(cudaMemcpyAsync(counts, dC, size_t(n_queries) * 8, cudaMemcpyDeviceToHost, ix->stream));
+            RBE_CK(cudaStreamSynchronize(ix->stream));
+            return;
+        }
+        ix->ensure_host_out(ne);
         RBE_CK(cudaMemcpyAsync(ix->host_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToHost,
                                ix->stream));
         RBE_CK(cudaStreamSynchronize(ix->stream));
@@ -521,6 +554,21 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
             }
             counts[q] = c;
         }
+    });
+}
+
+int rbe_cuda_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArgument("rbe_cuda_host_alloc: null output");
+        *out = nullptr;
+        if (bytes == 0) return;
+        RBE_CK(cudaMallocHost(out, bytes));
+    });
+}
+
+int rbe_cuda_host_free(void* p) {
+    return guarded([&] {
+        if (p) RBE_CK(cudaFreeHost(p));
     });
 }
 

@@ -85,5 +85,8 @@ size_t exact_queue_scratch_bytes(const ScanArgs& a);
 void launch_select_topn(const Result* d_in, const unsigned long long* d_counts, uint64_t cap, uint32_t Q,
                         uint64_t n, Result* d_out, void* d_scratch, size_t scratch_bytes, cudaStream_t st);
 size_t select_scratch_bytes(uint32_t Q, uint64_t cap, uint64_t n);
+// Result records -> caller SoA arrays (device or pinned host memory), counts per query.
+void launch_results_to_soa(const Result* d_in, uint32_t Q, uint64_t n, double* S, uint64_t* I, uint32_t* P,
+                           int64_t* A, uint64_t* C, cudaStream_t st);
 
 }  // namespace rbe_dev

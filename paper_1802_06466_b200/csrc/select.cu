@@ -278,7 +278,34 @@ __global__ void __launch_bounds__(kThreads) select_topn_kernel(const Result* __r
     }
 }
 
+// Result records [Q][n] -> the caller's structure-of-arrays layout (entries past a
+// query's count zeroed, counts = valid prefix length): one thread per entry.
+__global__ void results_to_soa_kernel(const Result* __restrict__ in, uint32_t Q, uint64_t n, double* __restrict__ S,
+                                      uint64_t* __restrict__ I, uint32_t* __restrict__ P, int64_t* __restrict__ A,
+                                      uint64_t* __restrict__ C) {
+    const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= uint64_t(Q) * n) return;
+    const Result r = in[e];
+    const bool v = r.valid != 0;
+    S[e] = v ? r.score : 0.0;
+    I[e] = v ? r.id : 0;
+    P[e] = v ? r.partition : 0;
+    if (A) A[e] = v ? r.acc : 0;
+    // the valid entries of a query are a prefix: its count is where valid flips
+    const uint64_t k = e % n;
+    if (v && (k + 1 == n || !in[e + 1].valid)) C[e / n] = k + 1;
+    if (k == 0 && !v) C[e / n] = 0;
+}
+
 }  // namespace
+
+void launch_results_to_soa(const Result* d_in, uint32_t Q, uint64_t n, double* S, uint64_t* I, uint32_t* P,
+                           int64_t* A, uint64_t* C, cudaStream_t st) {
+    const uint64_t total = uint64_t(Q) * n;
+    if (total == 0) return;
+    results_to_soa_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(d_in, Q, n, S, I, P, A, C);
+    RBE_CK(cudaGetLastError());
+}
 
 size_t select_scratch_bytes(uint32_t Q, uint64_t cap, uint64_t n) {
     (void)cap;

@@ -267,6 +267,15 @@ def test_search_words_out_buffers(rbe, port):
         for a, b, o in zip(got[:5], want[:5], out):
             assert a is o
             assert np.array_equal(a, b)
+    # page-locked out arrays: results are DMA'd straight into them
+    pe = rbe.pinned_empty
+    pinned = (pe((5, n), np.float64), pe((5, n), np.uint64), pe((5, n), np.uint32), pe((5, n), np.int64),
+              pe(5, np.uint64))
+    for arr in pinned:
+        arr.fill(3)
+    got = dix.search_words(qs, g, n, "auto", 0, False, pinned)
+    for a, b in zip(got[:5], want[:5]):
+        assert np.array_equal(a, b)
     with pytest.raises(ValueError):
         dix.search_words(qs, g, n, "auto", 0, False, out[:4])
     with pytest.raises(ValueError):
