@@ -536,24 +536,27 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
             RBE_CK(cudaStreamSynchronize(ix->stream));
             return;
         }
-        ix->ensure_host_out(ne);
-        RBE_CK(cudaMemcpyAsync(ix->host_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToHost,
-                               ix->stream));
+        // pageable caller buffers: the same device-side conversion, one D2H into pinned staging,
+        // then contiguous copies (no per-record scatter on the host)
+        const size_t b8 = ne * 8, b4 = ne * 4;
+        ix->soa.ensure(3 * b8 + b4 + size_t(n_queries) * 8 + 256);
+        uint8_t* base = static_cast<uint8_t*>(ix->soa.p);
+        double* dS = reinterpret_cast<double*>(base);
+        uint64_t* dI = reinterpret_cast<uint64_t*>(base + b8);
+        int64_t* dA = reinterpret_cast<int64_t*>(base + 2 * b8);
+        uint64_t* dC = reinterpret_cast<uint64_t*>(base + 3 * b8);
+        uint32_t* dP = reinterpret_cast<uint32_t*>(base + 3 * b8 + size_t(n_queries) * 8);
+        launch_results_to_soa(ix->out.as<Result>(), n_queries, n, dS, dI, dP, accs ? dA : nullptr, dC, ix->stream);
+        const size_t total = 3 * b8 + b4 + size_t(n_queries) * 8;
+        ix->ensure_host_out((total + sizeof(Result) - 1) / sizeof(Result));
+        uint8_t* h = reinterpret_cast<uint8_t*>(ix->host_out);
+        RBE_CK(cudaMemcpyAsync(h, base, total, cudaMemcpyDeviceToHost, ix->stream));
         RBE_CK(cudaStreamSynchronize(ix->stream));
-        for (uint32_t q = 0; q < n_queries; ++q) {
-            uint64_t c = 0;
-            for (uint64_t k = 0; k < n; ++k) {
-                const Result& r = ix->host_out[size_t(q) * n + k];
-                if (!r.valid) break;
-                const size_t o = size_t(q) * n + k;
-                scores[o] = r.score;
-                ids[o] = r.id;
-                partitions[o] = r.partition;
-                if (accs) accs[o] = r.acc;
-                ++c;
-            }
-            counts[q] = c;
-        }
+        std::memcpy(scores, h, b8);
+        std::memcpy(ids, h + b8, b8);
+        if (accs) std::memcpy(accs, h + 2 * b8, b8);
+        std::memcpy(counts, h + 3 * b8, size_t(n_queries) * 8);
+        std::memcpy(partitions, h + 3 * b8 + size_t(n_queries) * 8, b4);
     });
 }
 
