@@ -1,32 +1,40 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 exhaustive RBE retrieval path (BASELINE.json metric).
+"""Benchmark of the B200 exhaustive RBE retrieval path (BASELINE.json metric:
+"queries/s & p50 latency, top-1000 over 1B RBE docs; HBM GB/s vs peak").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (N=1): BASELINE config 2 -- 100M synthetic docs, 128-dim RBE with 3
-bit-planes (qp = kp = 3, residual weights), a 64-query batch, top-1000, one
-partition, default geometry (T_b=256, I=256, queue length 1, auto blocks).
-A step = one batch of 64 queries scanned over the whole corpus + selection.
-N>1 (torchrun, one process per GPU, NCCL): weak scaling, 100M docs per GPU
-(partition p on rank p), per-rank top-1000 gathered to rank 0 with one NCCL
-gather and merged on its GPU.
+Workload (BASELINE config 3, the metric's own): 1B synthetic docs, 128-dim RBE
+with 3 bit-planes (qp = kp = 3, residual weights), P = 8 partitions (doc i ->
+partition i mod 8, slot i div 8), a 64-query batch, top-1000, default geometry
+(T_b=256, I=256, queue length 1, auto blocks = ceil(125M / 65536) = 1908).
+It fits one B200 (60 GB with ids).  A step = one batch of 64 queries scanned
+over the whole corpus + selection (+ NCCL gather and device merge for N > 1).
 
-`value`  queries/s with the query batch already in HBM (device-timed, CUDA
-         events on the launching stream, max over ranks).
-`e2e`    the same through the public host API (DeviceIndex.search_words ->
-         rbe_cuda_search) with host buffers: H2D of the query words and D2H of
-         the result records inside the timed region.
-The corpus (5.2 GB per GPU) is larger than L2 (126 MB), so no L2 flush is
-needed between steps.
+Strong scaling: partition p lives on rank p mod N (N in {1, 2, 4, 8}); every N
+computes the identical merged top-1000 (its sha256 is in the JSON line as
+`result_sha256`, so runs at different N can be compared).
 
-`--impl reference` times the reference's own CPU rbe::search (compiled
-unmodified into oracle/_ref) on the host cores, query-parallel over all
-threads, on a bounded sample (a prefix of the same corpus), scaled linearly to
-the full corpus (the scan is O(N)).
+`value`  queries/s with the query batch already in HBM (CUDA events on the
+         launching stream, max over ranks).
+`e2e`    the same with host buffers: N=1 through the public API
+         (DeviceIndex.search_words -> rbe_cuda_search, page-locked out arrays);
+         N>1 H2D of the query words on every rank + the sharded device path +
+         D2H of the merged records on rank 0, host-timed, max over ranks.
+The corpus (52 GB) is far larger than L2 (126 MB): no flush is needed.
+
+`--impl reference` times the reference's own CPU rbe::search (its unmodified
+sources compiled into oracle/_ref) on the host cores on a bounded sample of the
+same workload: the first --sample-docs slots of partition 0 of the 1B-doc
+corpus, one query per host thread (query-parallel), scaled linearly to the
+whole corpus (the scan is O(N)); plus the reference "as
+shipped" (one rbe::search per query, sequentially, P=1 and P=nproc partitions
+of the sample -- std::async per partition).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -37,8 +45,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DIM, KP, QP, Q, K_TOP = 128, 3, 3, 64, 1000
-DOCS_PER_GPU = 100_000_000
+DIM, KP, QP = 128, 3, 3
 SEED_DOCS, SEED_QUERIES = 0xD0C5, 0x0E1
 METRIC = "queries/s & p50 latency, top-1000 over 1B RBE docs; HBM GB/s vs peak"
 UNIT = "queries/s"
@@ -50,16 +57,24 @@ def env_rank():
         os.environ.get("LOCAL_RANK", "0"))
 
 
-def workload(n_gpus, docs_per_gpu):
+def part_count(n_docs, P, p):
+    return (n_docs - p + P - 1) // P if p < n_docs else 0
+
+
+def workload(args, n_gpus):
+    per_part = part_count(args.docs, args.partitions, 0)
+    name = "BASELINE config 3" if args.docs == 1_000_000_000 and args.partitions == 8 else "custom"
     return {
-        "workload": f"BASELINE config 2 per GPU: {docs_per_gpu // 1_000_000}M docs x {DIM}-dim RBE, "
-                    f"{KP}+{QP} bit-planes (residual weights), Q={Q}, k={K_TOP}, geometry 256/256/1 auto blocks",
-        "docs": docs_per_gpu * n_gpus, "docs_per_gpu": docs_per_gpu, "dim": DIM, "keyword_planes": KP,
-        "query_planes": QP, "queries_per_batch": Q, "k": K_TOP, "partitions": n_gpus,
+        "workload": f"{name}: {args.docs / 1e9:g}B docs x {DIM}-dim RBE, {KP}+{QP} bit-planes (residual weights), "
+                    f"P={args.partitions} partitions (partition p on GPU p mod N), Q={args.queries}, k={args.k}, "
+                    f"geometry 256/256/1 auto blocks",
+        "docs": args.docs, "partitions": args.partitions, "docs_per_partition": per_part, "dim": DIM,
+        "keyword_planes": KP, "query_planes": QP, "queries_per_batch": args.queries, "k": args.k,
         "geometry": {"threads_per_block": 256, "items_per_thread": 256, "queue_length": 1,
-                     "blocks": -(-docs_per_gpu // 65536)},
+                     "blocks": -(-per_part // 65536)},
         "seeds": {"docs": SEED_DOCS, "queries": SEED_QUERIES},
-        "l2": "corpus 5.2 GB/GPU > 126 MB L2: inputs larger than L2, no flush",
+        "parallelism": f"shard{n_gpus} (partitions over GPUs, NCCL gather + device merge)",
+        "l2": f"corpus {args.docs * BYTES_PER_DOC / 1e9:.0f} GB > 126 MB L2: inputs larger than L2, no flush",
     }
 
 
@@ -125,7 +140,7 @@ def measured_peak():
 
 
 def ncu_traffic():
-    """dram bytes per scan launch from the committed `ncu --set full` summary."""
+    """dram bytes per main-scan launch from the committed `ncu --set full` summary."""
     try:
         with open(os.path.join(ROOT, "profiles", "scan_traffic.json")) as f:
             return json.load(f)
@@ -133,61 +148,89 @@ def ncu_traffic():
         return None
 
 
-# --------------------------------------------------------------------------- CPU reference arm
-def cpu_reference(steps, warmup, sample_docs=None, threads=None):
-    """The reference's rbe::search (oracle/_ref, unmodified sources) on a
-    bounded prefix sample; returns (qps scaled to the full 100M corpus, info)."""
-    import numpy as np
-
-    from oracle.oracle import Port, Ref, gen_queries, synthetic_prefix
-
-    threads = threads or os.cpu_count() or 1
-    sample_docs = sample_docs or 1_000_000
-    ref = Ref()
-    planes, mags, ids = synthetic_prefix(SEED_DOCS, DOCS_PER_GPU, sample_docs, DIM, KP, True, Port())
-    ix = ref.index(DIM, KP, True, [(planes, mags, ids)])
-    geo = (-(-sample_docs // 65536), 256, 256, 1)
-    qs = gen_queries(SEED_QUERIES, max(threads, 1), DIM, QP)
-    times = []
-    for s in range(warmup + steps):
-        t0 = time.perf_counter()
-        ix.search(qs, geo, K_TOP, threads=threads)
-        dt = time.perf_counter() - t0
-        if s >= warmup:
-            times.append(dt)
-    per_step = statistics.median(times)
-    qps_sample = qs.shape[0] / per_step
-    qps_full = qps_sample * sample_docs / DOCS_PER_GPU
-    import platform
-
-    cpu = platform.processor() or "cpu"
+def host_cpu():
     try:
         for line in open("/proc/cpuinfo"):
             if line.startswith("model name"):
-                cpu = line.split(":", 1)[1].strip()
-                break
+                return line.split(":", 1)[1].strip()
     except OSError:
         pass
-    info = {"value": qps_full, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{qs.shape[0]} queries per step (one per thread) over the first {sample_docs:,} docs of the "
-                      f"100M-doc corpus (P=1, same geometry rule), scaled x{sample_docs / DOCS_PER_GPU:g} to the full "
-                      f"corpus; {steps} steps, median {per_step * 1e3:.1f} ms/step; rbe::search from the reference's "
-                      f"own sources (oracle/_ref), query-parallel std::threads; host {cpu}",
-            "ms_per_step_sample": per_step * 1e3, "sample_docs": sample_docs}
-    return qps_full, info, times
+    import platform
+
+    return platform.processor() or "cpu"
+
+
+# --------------------------------------------------------------------------- CPU reference arm
+def cpu_reference(args, steps, warmup, as_shipped=True):
+    """The reference's rbe::search (oracle/_ref, its unmodified sources) on a bounded sample
+    of the workload: the first `sample_docs` slots of partition 0 of the corpus."""
+    import numpy as np
+
+    from oracle.oracle import Port, Ref, gen_queries
+
+    threads = os.cpu_count() or 1
+    S = min(args.sample_docs, part_count(args.docs, args.partitions, 0))
+    ref = Ref()
+    planes, mags, ids = Port().gen_partition_prefix(SEED_DOCS, args.docs, DIM, KP, args.partitions, 0, S, threads)
+    ix = ref.index(DIM, KP, True, [(planes, mags, ids)])
+    geo = (-(-S // 65536), 256, 256, 1)
+    qs = gen_queries(SEED_QUERIES, max(threads, 1), DIM, QP)
+    scale = S / args.docs  # the scan is O(N): sample docs / whole corpus
+    times, cpu_times = [], []
+    for s in range(warmup + steps):
+        t0, c0 = time.perf_counter(), time.process_time()
+        ix.search(qs, geo, args.k, threads=threads)
+        dt, dc = time.perf_counter() - t0, time.process_time() - c0
+        if s >= warmup:
+            times.append(dt)
+            cpu_times.append(dc)
+    per_step = statistics.median(times)
+    qps = qs.shape[0] / per_step * scale
+    info = {"value": qps, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{qs.shape[0]} queries per step (one per host thread, query-parallel rbe::search) over the "
+                      f"first {S:,} slots of partition 0 of the {args.docs:,}-doc corpus ({S * BYTES_PER_DOC / 1e9:.2f} "
+                      f"GB, >> LLC), scaled x{scale:g} to the whole corpus; {len(times)} steps, median "
+                      f"{per_step * 1e3:.0f} ms wall / {statistics.median(cpu_times) * 1e3:.0f} ms process CPU per step; "
+                      f"reference sources compiled unmodified (oracle/_ref); host {host_cpu()}",
+            "ms_per_step_sample": per_step * 1e3, "cpu_ms_per_step_sample": statistics.median(cpu_times) * 1e3,
+            "sample_docs": S, "ns_per_doc_query_thread": per_step * 1e9 / S}
+    if as_shipped:
+        # the reference as shipped: one rbe::search per query, sequentially (CLI semantics,
+        # tools/rbe_main.cpp:185-199), P=1 and P=nproc partitions (std::async per partition)
+        shipped = {}
+        for P in (1, threads):
+            if P == 1:
+                pix = ix
+            else:
+                w = planes.reshape(KP, S, -1)
+                pparts = []
+                for p in range(P):
+                    sel = np.arange(p, S, P)
+                    pparts.append((np.ascontiguousarray(w[:, sel]).reshape(KP, -1), mags[sel], ids[sel]))
+                pix = ref.index(DIM, KP, True, pparts)
+            pgeo = (-(-(-(-S // P)) // 65536), 256, 256, 1)
+            t0, c0 = time.perf_counter(), time.process_time()
+            nq = 2
+            for q in range(nq):
+                pix.search(qs[q:q + 1], pgeo, args.k, threads=1)
+            dt, dc = time.perf_counter() - t0, time.process_time() - c0
+            shipped[f"P={P}"] = {"value": nq / dt * scale, "unit": UNIT, "wall_ms_per_query_sample": dt / nq * 1e3,
+                                 "cpu_ms_per_query_sample": dc / nq * 1e3}
+        info["as_shipped"] = shipped
+    return qps, info, times
 
 
 def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    qps, info, times = cpu_reference(args.steps, args.warmup, args.sample_docs)
+    qps, info, times = cpu_reference(args, args.steps, args.warmup)
     line = {
         "metric": METRIC, "value": qps, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64 popcnt -> s64 acc, f64 score",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64 popcnt -> s64 acc, f64 score",
         "data": "synthetic (counter-based splitmix64 corpus, SURVEY.md §8(d))",
-        "config": workload(args.gpus, DOCS_PER_GPU), "cpu_baseline": info,
+        "config": workload(args, args.gpus), "cpu_baseline": info,
         "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -200,135 +243,194 @@ def run_ours(args):
     import torch
 
     import paper_1802_06466_b200 as rbe
-    from oracle.oracle import gen_queries  # the query generator (same as the corpus stream)
+    from oracle.oracle import gen_queries  # the query generator (same counter stream as the corpus)
+    from paper_1802_06466_b200.distributed import RESULT_BYTES, gather_and_merge
 
     rank, world, local = env_rank()
-    n_gpus = world
     torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    docs_per_gpu = args.docs_per_gpu
-    n_docs = docs_per_gpu * world
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+    Q, K = args.queries, args.k
     t_build = time.perf_counter()
-    dix = rbe.DeviceIndex.synthetic(DIM, KP, True, n_docs, world, SEED_DOCS, [local], rank, world)
+    # partitions p with p % world == rank, generated on this GPU
+    dix = rbe.DeviceIndex.synthetic(DIM, KP, True, args.docs, args.partitions, SEED_DOCS, [local], rank, world)
+    torch.cuda.synchronize()
     build_s = time.perf_counter() - t_build
     geo = rbe.ScanGeometry()
-    geo.blocks = -(-dix.max_partition_count // 65536)
+    geo.blocks = -(-part_count(args.docs, args.partitions, 0) // 65536)
     qs = gen_queries(SEED_QUERIES, Q, DIM, QP)
-    d_words = torch.from_numpy(qs.view(np.int64).copy()).to(f"cuda:{local}")
-    from paper_1802_06466_b200.distributed import RESULT_BYTES, gather_and_merge
-
+    d_words = torch.from_numpy(qs.view(np.int64).copy()).to(dev)
     # a dedicated stream (the legacy default stream's handle is 0, which the C ABI reads as
     # "the index's own stream"): every kernel, copy and event of a step is ordered on it
-    stream = torch.cuda.Stream(device=f"cuda:{local}")
+    stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    out = torch.empty(Q * K_TOP * RESULT_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+    out = torch.empty(Q * K * RESULT_BYTES, dtype=torch.uint8, device=dev)
+    merged = torch.empty_like(out)
+    gathered = torch.empty(world * Q * K * RESULT_BYTES, dtype=torch.uint8, device=dev) if rank == 0 else None
+    has_docs = dix.total_keywords > 0
 
     def merge(blocks):
         if len(blocks) == 1:
             return blocks[0]
-        cat = torch.cat(blocks)
-        merged = torch.empty_like(blocks[0])
-        rbe.merge_device(local, cat.data_ptr(), len(blocks), Q, K_TOP, merged.data_ptr(), stream.cuda_stream)
+        torch.cat(blocks, out=gathered)
+        rbe.merge_device(local, gathered.data_ptr(), len(blocks), Q, K, merged.data_ptr(), stream.cuda_stream)
         return merged
 
     def step(with_stats):
         # with_stats=False: the batch is only enqueued (no host sync), so consecutive
         # steps run back to back on the GPU
-        st = rbe.search_device(dix.handle(0), d_words.data_ptr(), Q, QP, geo, K_TOP, out.data_ptr(),
-                               stream.cuda_stream, args.variant, with_stats)
-        gather_and_merge(out, rank, world, merge, dist)
-        return st
+        st = None
+        if has_docs:
+            st = rbe.search_device(dix.handle(0), d_words.data_ptr(), Q, QP, geo, K, out.data_ptr(),
+                                   stream.cuda_stream, args.variant, with_stats)
+        else:
+            out.zero_()
+        return st, gather_and_merge(out, rank, world, merge, dist)
 
     stats = []
     for _ in range(args.warmup):
-        stats.append(step(True))  # warm-up steps also collect the per-batch counters
+        st, _ = step(True)  # warm-up steps also collect the per-batch counters
+        if st:
+            stats.append(st)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    scan_ms_timed = []
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         ev[0].record(stream)
+        res = None
         for s in range(args.steps):
-            step(False)
+            _, res = step(False)
             ev[s + 1].record(stream)
         torch.cuda.synchronize()
-        scan_ms_timed.append(rbe.last_batch_ms(dix.handle(0))[0])  # the last timed batch's scan kernels
     if dist:
         dist.barrier()
     per = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[args.steps])
+    if has_docs:
+        rbe.last_batch_ms(dix.handle(0))  # surfaces a sticky error of any asynchronous batch
     if dist:
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = Q * args.steps / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (the scan): algorithmic bytes / its event time, from the
-    # CUDA events the library records around the scan kernels of the last timed batch
-    scan_ms = statistics.mean(scan_ms_timed)
-    scan_bytes = dix.scan_bytes  # this rank's docs x 52 B
-    peak, peak_src = measured_peak()
-    achieved = scan_bytes / (scan_ms / 1e3) / 1e9
-    traffic = ncu_traffic()
-    launches = int(stats[-1]["launches"]) * args.steps + (args.steps if world > 1 and rank == 0 else 0)
+    # identical-results check across N: sha256 of the merged records (score, id, partition)
+    digest = None
+    if rank == 0:
+        rec = np.frombuffer(res.cpu().numpy().tobytes(), dtype=np.dtype(
+            [("score", "<f8"), ("id", "<u8"), ("acc", "<i8"), ("partition", "<u4"), ("valid", "<u4")]))
+        digest = hashlib.sha256(rec[["score", "id", "partition", "valid"]].tobytes()).hexdigest()
+        n_valid = int(rec["valid"].sum())
 
-    # e2e through the public host API with host buffers (N=1: rbe_cuda_search)
+    # roofline of the dominant kernel (the scan): this rank's algorithmic bytes / the scan
+    # kernels' device time (CUDA events around probe + threshold + main scan on the launching
+    # stream), averaged over `steps` further batches with per-batch statistics
+    scan_ms = []
+    if has_docs:
+        for _ in range(args.steps):
+            st, _ = step(True)
+            scan_ms.append(st["scan_ms"])
+    scan_ms = statistics.mean(scan_ms) if scan_ms else float("nan")
+    scan_bytes = dix.scan_bytes
+    peak, peak_src = measured_peak()
+    achieved = scan_bytes / (scan_ms / 1e3) / 1e9 if has_docs else 0.0
+    if dist:
+        t = torch.tensor([achieved, scan_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)  # the slowest rank
+        achieved, scan_ms = float(t[0].item()), float(t[1].item())
+    traffic = ncu_traffic()
+    launches = (int(stats[-1]["launches"]) if stats else 0) * args.steps + (2 * args.steps if world > 1 and rank == 0
+                                                                            else 0)
+
+    # e2e with host buffers
     e2e = None
     if world == 1:
-        # a serving loop: the result arrays are allocated once and reused (out=), the query
-        # words come from host memory and the results land in host memory every batch
-        pe = rbe.pinned_empty  # page-locked, as a serving loop would hold them
-        out = (pe((Q, K_TOP), np.float64), pe((Q, K_TOP), np.uint64), pe((Q, K_TOP), np.uint32),
-               pe((Q, K_TOP), np.int64), pe(Q, np.uint64))
+        # a serving loop through the public API: the result arrays are allocated once
+        # (page-locked) and reused (out=); the query words come from host memory and the
+        # results land in host memory every batch
+        pe = rbe.pinned_empty
+        outs = (pe((Q, K), np.float64), pe((Q, K), np.uint64), pe((Q, K), np.uint32), pe((Q, K), np.int64),
+                pe(Q, np.uint64))
         for _ in range(2):
-            dix.search_words(qs, geo, K_TOP, args.variant, 0, False, out)
-        t0 = time.perf_counter()
+            dix.search_words(qs, geo, K, args.variant, 0, False, outs)
         e2e_times = []
+        t0 = time.perf_counter()
         for _ in range(args.steps):
             t1 = time.perf_counter()
-            dix.search_words(qs, geo, K_TOP, args.variant, 0, False, out)
+            dix.search_words(qs, geo, K, args.variant, 0, False, outs)
             e2e_times.append(time.perf_counter() - t1)
         e2e_total = time.perf_counter() - t0
         e2e = {"value": Q * args.steps / e2e_total, "unit": UNIT, "h2d_bytes_per_step": int(qs.nbytes),
-               "d2h_bytes_per_step": Q * K_TOP * (8 + 8 + 4 + 8) + Q * 8, "p50_ms": statistics.median(e2e_times) * 1e3,
+               "d2h_bytes_per_step": Q * K * (8 + 8 + 4 + 8) + Q * 8, "p50_ms": statistics.median(e2e_times) * 1e3,
                "api": "DeviceIndex.search_words(out=reused page-locked host arrays) -> rbe_cuda_search"}
+    else:
+        h_words = torch.from_numpy(qs.view(np.int64).copy()).pin_memory()
+        h_res = torch.empty(Q * K * RESULT_BYTES, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            d_words.copy_(h_words, non_blocking=True)
+            _, r = step(False)
+            if rank == 0:
+                h_res.copy_(r, non_blocking=True)
+            stream.synchronize()
+
+        for _ in range(2):
+            e2e_step()
+        dist.barrier()
+        e2e_times = []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            t1 = time.perf_counter()
+            e2e_step()
+            e2e_times.append(time.perf_counter() - t1)
+        e2e_total = time.perf_counter() - t0
+        t = torch.tensor([e2e_total, statistics.median(e2e_times)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": Q * args.steps / float(t[0].item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(qs.nbytes) * world, "d2h_bytes_per_step": Q * K * RESULT_BYTES,
+               "p50_ms": float(t[1].item()) * 1e3,
+               "api": "per rank: H2D query words -> rbe_cuda_search_device; NCCL gather; rbe_cuda_merge_device; "
+                      "D2H of the merged records on rank 0"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            _, cpu, _ = cpu_reference(steps=2, warmup=0, sample_docs=args.sample_docs * 4)
+            _, cpu, _ = cpu_reference(args, steps=1, warmup=0)
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "kind": "reference", "error": str(ex)}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "p50_ms": statistics.median(per),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "s8xu8->s32 tensor / u32 popc->s64; f64 scores" if stats[0]["variant"] == "tensor"
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "s8xu8->s32 tensor / u32 popc->s64; f64 scores" if stats and stats[0]["variant"] == "tensor"
             else "u32 popc -> s64 acc, f64 score",
             "data": "synthetic (counter-based splitmix64 corpus generated on device, SURVEY.md §8(d))",
-            "config": dict(workload(n_gpus, docs_per_gpu), parallelism=f"shard{n_gpus}", variant=stats[0]["variant"]),
+            "config": dict(workload(args, world), variant=stats[0]["variant"] if stats else None),
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                         "kernel": "scan (" + stats[0]["variant"] + ")", "scan_ms": scan_ms,
-                         "algorithmic_bytes_per_launch": scan_bytes, "peak_source": peak_src,
-                         "aggregate_frac": (scan_bytes * n_gpus / (ms_per_step / 1e3) / 1e9) / (peak * n_gpus)},
+                         "traffic_config": traffic.get("config") if traffic else None,
+                         "kernel": "scan (" + (stats[0]["variant"] if stats else "-") + "): probe + threshold + main",
+                         "scan_ms": scan_ms, "algorithmic_bytes_per_launch": scan_bytes,
+                         "bytes_per_doc": BYTES_PER_DOC, "peak_source": peak_src,
+                         "aggregate_frac": (args.docs * BYTES_PER_DOC / (ms_per_step / 1e3) / 1e9) / (peak * world)},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
-            "doc_queries_per_s": value * n_docs,
+            "result_sha256": digest, "result_entries": n_valid,
+            "doc_queries_per_s": value * args.docs,
             "index_build_s": build_s,
-            "candidates_per_batch": statistics.mean(s["candidates"] for s in stats),
-            "survivors_per_batch": statistics.mean(s["survivors"] for s in stats),
+            "candidates_per_batch": statistics.mean(s["candidates"] for s in stats) if stats else None,
+            "survivors_per_batch": statistics.mean(s["survivors"] for s in stats) if stats else None,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -340,12 +442,15 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "exact", "tensor"])
-    ap.add_argument("--docs-per-gpu", type=int, default=DOCS_PER_GPU)
-    ap.add_argument("--sample-docs", type=int, default=1_000_000)
+    ap.add_argument("--docs", type=int, default=1_000_000_000)
+    ap.add_argument("--partitions", type=int, default=8)
+    ap.add_argument("--queries", type=int, default=64)
+    ap.add_argument("--k", type=int, default=1000)
+    ap.add_argument("--sample-docs", type=int, default=8_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -32,11 +32,13 @@ struct Candidate {
     uint64_t slot = 0;
 };
 
+// Layout-identical to the reference's SelectionEntry (search.hpp:34-38).  The exact
+// integer accumulator behind a score (score = ldexp(acc, -L) / magnitude) is returned
+// separately (DeviceIndex::search_words' `accs`).
 struct SelectionEntry {
     double score = 0.0;
     uint64_t id = 0;
     uint32_t partition = 0;
-    int64_t acc = 0;  // exact integer accumulator: score = ldexp(acc, -L) / magnitude
 };
 
 struct SelectionResult {
@@ -78,11 +80,13 @@ public:
     /// Copy local partition back in the reference layout (tests).
     Partition download_partition(uint32_t partition) const;
 
-    /// Raw batched call: queries [Q][qp][wpp] words -> per-query results.
+    /// Raw batched call: queries [Q][qp][wpp] words -> per-query results; `accs` (optional)
+    /// receives each entry's exact integer accumulator, parallel to the entries.
     std::vector<SelectionResult> search_words(std::span<const uint64_t> query_words, uint32_t n_queries,
                                               uint32_t query_planes, const ScanGeometry& geometry, uint64_t n,
                                               SearchStats* stats = nullptr, ScanVariant variant = ScanVariant::Auto,
-                                              uint32_t probe_tiles = 0) const;
+                                              uint32_t probe_tiles = 0,
+                                              std::vector<std::vector<int64_t>>* accs = nullptr) const;
     /// Same, writing into caller-owned [Q][n] arrays (counts[Q] valid entries per query);
     /// stats may be null (then the batch runs with a single host synchronisation).
     void search_words_into(std::span<const uint64_t> query_words, uint32_t n_queries, uint32_t query_planes,
@@ -91,6 +95,9 @@ public:
                            ScanVariant variant = ScanVariant::Auto, uint32_t probe_tiles = 0) const;
     rbe_cuda_index* handle(size_t i) const { return handles_.at(i).get(); }
     size_t handle_count() const { return handles_.size(); }
+    /// (handle index, local slot) of a resident global partition; throws out_of_range otherwise.
+    std::pair<size_t, uint32_t> locate(uint32_t partition) const;
+    uint64_t partition_size(uint32_t partition) const;
 
 private:
     DeviceIndex() = default;
@@ -107,6 +114,22 @@ private:
     std::vector<uint32_t> part_local_;
     std::vector<uint64_t> part_count_;
 };
+
+/// local_select (reference search.hpp:53-57) on the device: the per-logical-thread
+/// candidate lists of one partition, indexed by block * threads_per_block + thread, each
+/// ordered by (score desc, slot asc).  The KeywordIndex overload uploads that partition
+/// for the call.
+std::vector<std::vector<Candidate>> local_select(const RbeEmbedding& query, const DeviceIndex& index,
+                                                 uint32_t partition, const ScanGeometry& geometry,
+                                                 SearchStats* stats = nullptr);
+std::vector<std::vector<Candidate>> local_select(const RbeEmbedding& query, const KeywordIndex& index,
+                                                 uint32_t partition, const ScanGeometry& geometry,
+                                                 SearchStats* stats = nullptr);
+
+/// global_select (reference search.hpp:61-63): the best n of one partition's surviving
+/// candidates under (score desc, id asc), selected on the device.
+SelectionResult global_select(const std::vector<std::vector<Candidate>>& per_thread, const Partition& partition,
+                              uint32_t partition_ordinal, uint64_t n);
 
 /// rbe::search on the device store.
 SelectionResult search(const RbeEmbedding& query, const DeviceIndex& index, const ScanGeometry& geometry, uint64_t n,

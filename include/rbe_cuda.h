@@ -21,6 +21,19 @@
  *   rbe_cuda_merge_device     the final merge under entry_less
  *                             (search.cpp:50-53, 160-167) over gathered lists.
  *
+ *   rbe_cuda_local_select     local_select (search.hpp:53-57, search.cpp:57-113):
+ *                             per-logical-thread candidate lists of one partition.
+ *   rbe_cuda_select_topn      global_select's sort + truncate (search.cpp:115-128).
+ *
+ * Streams and lifetime: every call may be issued on any stream; an index orders
+ * its batches across streams itself (the next batch waits for the previous one),
+ * and all scratch is owned by the index (or, for merge/select, by a per-device
+ * context) and reused across calls -- no per-call device allocation in steady
+ * state.  The tensor kernel's internal-consistency flag is sticky per index: a
+ * batch enqueued asynchronously (search_device without stats) that trips it is
+ * reported by the next synchronous call on that index (rbe_cuda_search,
+ * search_device with stats, last_batch_ms, rbe_cuda_index_check, search_multi).
+ *
  * Error model (mirrors the reference's exceptions):
  *   RBE_CUDA_EINVAL   -> std::invalid_argument / ValueError
  *   RBE_CUDA_ERANGE   -> std::out_of_range     / IndexError
@@ -167,14 +180,43 @@ int rbe_cuda_host_free(void* ptr);
 
 /* Merge `n_lists` result lists per query (d_in = rbe_result[n_lists][n_queries][n],
  * device memory on `device`) into the top n per query under (score desc,
- * id asc): d_out = rbe_result[n_queries][n]. */
+ * id asc): d_out = rbe_result[n_queries][n].  Asynchronous: enqueued on `stream`
+ * (NULL = a per-device stream) with persistent per-device scratch. */
 int rbe_cuda_merge_device(int device, const rbe_result* d_in, uint32_t n_lists, uint32_t n_queries,
                           uint64_t n, rbe_result* d_out, void* stream);
 
-/* Single-process multi-GPU rbe::search: each handle (one per device) scans its
- * partitions into a device-resident top n, the lists are copied peer-to-peer
- * to handles[0]'s device and merged there (rbe_cuda_merge_device); host
- * outputs as in rbe_cuda_search.  stats->scored sums over handles. */
+/* local_select (search.hpp:53-57) of local partition `i` for one query
+ * (query_words = [query_planes][words_per_plane] u64): for every logical thread
+ * t = block * threads_per_block + thread, its best min(queue_length,
+ * items_per_thread) candidates under (score desc, slot asc) in
+ * scores/slots[t * ql .. t * ql + counts[t]) (ql = min(queue_length,
+ * items_per_thread); buffers hold blocks * threads_per_block * ql entries and
+ * counts blocks * threads_per_block).  *scored += keywords scored. */
+int rbe_cuda_local_select(rbe_cuda_index* index, uint32_t i, const uint64_t* query_words, uint32_t query_planes,
+                          const rbe_scan_geometry* geometry, double* scores, uint64_t* slots, uint32_t* counts,
+                          uint64_t* scored);
+
+/* global_select's selection (search.cpp:115-128) on device `device`: the top n of
+ * `count` (score, id) candidates under (score desc, id asc); host buffers in and
+ * out, *out_count = min(n, count). */
+int rbe_cuda_select_topn(int device, const double* scores, const uint64_t* ids, uint64_t count, uint32_t partition,
+                         uint64_t n, double* out_scores, uint64_t* out_ids, uint64_t* out_count);
+
+/* Waits for the index's last batch and reports its sticky internal-consistency
+ * flag (RBE_CUDA_ERUNTIME if any batch since the last report tripped it). */
+int rbe_cuda_index_check(rbe_cuda_index* index);
+
+/* Test hook: sets the index's sticky internal-consistency flag, as a failed
+ * accumulator recovery in the tensor kernel would. */
+int rbe_cuda_index_inject_error(rbe_cuda_index* index);
+
+/* Single-process multi-GPU rbe::search: every handle (one per device) scans its
+ * partitions into a device-resident top n -- all devices concurrently, each on
+ * its own stream -- then the lists are copied peer-to-peer to the first
+ * non-empty handle's device and merged there; host outputs as in
+ * rbe_cuda_search.  Handles without documents take no part; only an index
+ * whose handles are all empty is rejected (search.cpp:133-135).
+ * stats->scored sums over handles. */
 int rbe_cuda_search_multi(rbe_cuda_index* const* handles, uint32_t n_handles, const uint64_t* query_words,
                           uint32_t n_queries, uint32_t query_planes, const rbe_scan_geometry* geometry, uint64_t n,
                           const rbe_search_options* options, double* scores, uint64_t* ids, uint32_t* partitions,

@@ -117,6 +117,8 @@ class Ref:
                                        C.c_uint32]
         L.ref_partition_select.argtypes = [C.c_void_p, U64P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                            C.c_uint32, C.c_uint32, C.c_uint64, F64P, U64P, U32P, U64P, U64P]
+        L.ref_local_select.argtypes = [C.c_void_p, U64P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.c_uint32, C.c_uint32, F64P, U64P, U32P, U64P]
         L.ref_pack.argtypes = [C.POINTER(C.c_int), C.c_uint32, U64P, U32P]
         L.ref_binary_dot.argtypes = [U64P, C.c_uint32, U64P, C.c_uint32, I64P]
         L.ref_combine_plane_dots.restype = C.c_double
@@ -256,6 +258,22 @@ class RefIndex:
             out.append(list(zip(scores[s].tolist(), ids[s].tolist(), parts[s].tolist())))
         return out, scored.value
 
+    def local_select(self, query, p, geometry):
+        """rbe::local_select -> (scores[threads][ql], slots[threads][ql], counts[threads], scored),
+        ql = min(queue_length, items_per_thread)."""
+        q = np.ascontiguousarray(query, dtype=np.uint64)
+        b, t, i, ql = geometry
+        qle = min(ql, i)
+        threads = b * t
+        scores = np.zeros((threads, qle), dtype=np.float64)
+        slots = np.zeros((threads, qle), dtype=np.uint64)
+        counts = np.zeros(threads, dtype=np.uint32)
+        scored = C.c_uint64()
+        self.ref._check(self.ref.L.ref_local_select(self.h, _p(q, U64P), q.shape[0], p, b, t, i, ql, qle,
+                                                    _p(scores, F64P), _p(slots, U64P), _p(counts, U32P),
+                                                    C.byref(scored)))
+        return scores, slots, counts, scored.value
+
     def partition_select(self, query, p, geometry, n):
         q = np.ascontiguousarray(query, dtype=np.uint64)
         b, t, i, ql = geometry
@@ -296,6 +314,10 @@ class Port:
         L.rbo_magnitude.restype = C.c_double
         L.rbo_magnitude.argtypes = [U64P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int]
         L.rbo_partition_magnitudes.argtypes = [U64P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, F32P]
+        L.rbo_gen_partition_planes_range.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                     C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, U64P]
+        L.rbo_partition_magnitudes_range.argtypes = [U64P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                                                     C.c_uint32, C.c_int, F32P]
         L.rbo_thread_assignment.restype = C.c_uint32
         L.rbo_thread_assignment.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
                                             C.c_uint32, U64P]
@@ -316,6 +338,27 @@ class Port:
         out = np.zeros(kp * count * wpp, dtype=np.uint64)
         self.L.rbo_gen_partition_planes(seed, n_total, dim, kp, n_partitions, p, count, _p(out, U64P))
         return out.reshape(kp, count * wpp)
+
+    def gen_partition_prefix(self, seed, n_total, dim, kp, n_partitions, p, count, threads=1):
+        """The first `count` slots of partition p (reference layout planes, exact magnitudes,
+        ids): a bounded sample of a large synthetic corpus, generated with `threads` threads."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        wpp = wpp_of(dim)
+        planes = np.empty(kp * count * wpp, dtype=np.uint64)
+        mags = np.empty(count, dtype=np.float32)
+        step = -(-count // max(threads, 1))
+
+        def chunk(b):
+            e = min(b + step, count)
+            self.L.rbo_gen_partition_planes_range(seed, n_total, dim, kp, n_partitions, p, count, b, e,
+                                                  _p(planes, U64P))
+            self.L.rbo_partition_magnitudes_range(_p(planes, U64P), count, b, e, dim, kp, int(True), _p(mags, F32P))
+
+        with ThreadPoolExecutor(max_workers=max(threads, 1)) as ex:  # ctypes releases the GIL
+            list(ex.map(chunk, range(0, count, step)))
+        ids = np.arange(count, dtype=np.uint64) * np.uint64(n_partitions) + np.uint64(p)
+        return planes.reshape(kp, count * wpp), mags, ids
 
     def gen_queries(self, seed, Q, dim, qp):
         out = np.zeros(Q * qp * wpp_of(dim), dtype=np.uint64)

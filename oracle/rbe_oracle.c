@@ -57,6 +57,25 @@ void rbo_gen_partition_planes(uint64_t seed, uint64_t n_total, uint32_t dim, uin
     }
 }
 
+/* Same for the slots [begin, end) only (parallel callers; planes laid out for `count`). */
+void rbo_gen_partition_planes_range(uint64_t seed, uint64_t n_total, uint32_t dim, uint32_t kp,
+                                    uint32_t n_partitions, uint32_t partition, uint64_t count,
+                                    uint64_t begin, uint64_t end, uint64_t* planes) {
+    const uint64_t wpp = (dim + 63) / 64;
+    const uint64_t pm = pad_mask(dim);
+    for (uint32_t t = 0; t < kp; ++t) {
+        uint64_t* block = planes + (uint64_t)t * count * wpp;
+        for (uint64_t s = begin; s < end; ++s) {
+            const uint64_t i = s * n_partitions + partition;
+            for (uint64_t w = 0; w < wpp; ++w) {
+                uint64_t v = rbo_splitmix64_at(seed, ((uint64_t)t * n_total + i) * wpp + w);
+                if (w + 1 == wpp) v &= pm;
+                block[s * wpp + w] = v;
+            }
+        }
+    }
+}
+
 /* Query q, plane s, word w = stream value (q*qp + s)*wpp + w, pad-masked. */
 void rbo_gen_queries(uint64_t seed, uint32_t n_queries, uint32_t dim, uint32_t qp, uint64_t* out) {
     const uint64_t wpp = (dim + 63) / 64;
@@ -124,6 +143,14 @@ void rbo_partition_magnitudes(const uint64_t* planes, uint64_t count, uint32_t d
                               int residual_weights, float* mags) {
     const uint64_t wpp = (dim + 63) / 64;
     for (uint64_t s = 0; s < count; ++s)
+        mags[s] = (float)rbo_magnitude(planes + s * wpp, count * wpp, dim, kp, residual_weights);
+}
+
+/* Same for the slots [begin, end) of a partition of `count` docs (parallel callers). */
+void rbo_partition_magnitudes_range(const uint64_t* planes, uint64_t count, uint64_t begin, uint64_t end,
+                                    uint32_t dim, uint32_t kp, int residual_weights, float* mags) {
+    const uint64_t wpp = (dim + 63) / 64;
+    for (uint64_t s = begin; s < end; ++s)
         mags[s] = (float)rbo_magnitude(planes + s * wpp, count * wpp, dim, kp, residual_weights);
 }
 

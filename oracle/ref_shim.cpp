@@ -234,6 +234,29 @@ int ref_partition_select(void* h, const uint64_t* query, uint32_t qp, uint32_t p
     })
 }
 
+// rbe::local_select alone (search.cpp:57-113): the per-thread candidate lists,
+// flattened to [threads][ql] (ql = the caller's stride) with counts[threads].
+int ref_local_select(void* h, const uint64_t* query, uint32_t qp, uint32_t p, uint32_t blocks, uint32_t tpb,
+                     uint32_t ipt, uint32_t queue_length, uint32_t ql, double* scores, uint64_t* slots,
+                     uint32_t* counts, uint64_t* scored) {
+    REF_TRY({
+        auto* idx = static_cast<rbe::KeywordIndex*>(h);
+        rbe::ScanGeometry g{blocks, tpb, ipt, queue_length};
+        rbe::RbeEmbedding e = make_query(query, qp, idx->dim);
+        rbe::SearchStats st;
+        auto lists = rbe::local_select(e, *idx, p, g, &st);
+        for (size_t t = 0; t < lists.size(); ++t) {
+            if (lists[t].size() > ql) throw std::logic_error("ref_local_select: list longer than the stride");
+            counts[t] = uint32_t(lists[t].size());
+            for (size_t k = 0; k < lists[t].size(); ++k) {
+                scores[t * ql + k] = lists[t][k].score;
+                slots[t * ql + k] = lists[t][k].slot;
+            }
+        }
+        if (scored) *scored = st.scored;
+    })
+}
+
 // Leaf functions (binary_vector.hpp:33-43, embedding.cpp:7-90, search.cpp:10-26).
 int ref_pack(const int* values, uint32_t n, uint64_t* words, uint32_t* dim) {
     REF_TRY({

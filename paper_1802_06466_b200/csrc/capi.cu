@@ -2,9 +2,20 @@
 // store) and the batched search orchestration (query upload, scan kernel,
 // device selection, result download).  No CPU fallback: every compute entry
 // point fails with RBE_CUDA_ERUNTIME when CUDA is unusable.
+//
+// Concurrency and lifetime rules (include/rbe_cuda.h):
+//  * every device buffer is owned (DevBuf frees itself) and per-batch scratch is
+//    grown on demand, never allocated per call in steady state;
+//  * a batch may be issued on any stream; each index records an event at the end
+//    of its last batch and the next batch's stream waits on it before touching
+//    the index's scratch, so batches on different streams never overlap;
+//  * the tensor kernel's internal-consistency flag is sticky: it is never cleared
+//    per batch, and the next synchronous call on the index (rbe_cuda_search,
+//    search_device with stats, last_batch_ms, search_multi) reports it.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -49,14 +60,31 @@ int guarded(F&& f) {
     }
 }
 
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
+// Owned device allocation, grown on demand (cudaFree synchronises the device,
+// so growing never races with in-flight work that used the old buffer).
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void ensure(size_t b) {
         if (b <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
+        release();
         if (b == 0) return;
         RBE_CK(cudaMalloc(&p, b));
         bytes = b;
@@ -70,6 +98,8 @@ struct DevBuf {
     T* as() const {
         return static_cast<T*>(p);
     }
+    void* p = nullptr;
+    size_t bytes = 0;
 };
 
 uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
@@ -85,6 +115,100 @@ struct DeviceGuard {
     }
 };
 
+// Device usability, checked once per device (cudaGetDeviceProperties is slow).
+constexpr int kMaxDevices = 64;
+void check_device_usable(int device) {
+    static std::once_flag count_once;
+    static int n_devices = 0;
+    static cudaError_t count_err = cudaSuccess;
+    std::call_once(count_once, [] { count_err = cudaGetDeviceCount(&n_devices); });
+    if (count_err != cudaSuccess || n_devices == 0)
+        throw CudaError(std::string("no usable CUDA device (") + cudaGetErrorString(count_err) +
+                        "); the RBE search path has no CPU fallback");
+    if (device < 0 || device >= n_devices || device >= kMaxDevices)
+        throw InvalidArgument("rbe_cuda: device ordinal out of range");
+    static std::mutex mu;
+    static std::array<int, kMaxDevices> major{};  // 0 = not yet queried
+    std::lock_guard<std::mutex> lk(mu);
+    if (major[device] == 0) {
+        cudaDeviceProp prop;
+        RBE_CK(cudaGetDeviceProperties(&prop, device));
+        major[device] = prop.major * 100 + prop.minor;
+    }
+    if (major[device] / 100 != 10)
+        throw CudaError("rbe_cuda: kernels are compiled for sm_100a (B200); device " + std::to_string(device) +
+                        " is sm_" + std::to_string(major[device]));
+}
+
+// Stream-ordered exclusive use of a set of scratch buffers: the stream of the next
+// user waits for the end of the previous user's work when it ran on another stream.
+struct StreamOrder {
+    cudaEvent_t done = nullptr;
+    cudaStream_t last = nullptr;
+    bool used = false;
+    void acquire(cudaStream_t st) {
+        if (used && last != st) RBE_CK(cudaStreamWaitEvent(st, done, 0));
+    }
+    void release(cudaStream_t st) {
+        RBE_CK(cudaEventRecord(done, st));
+        last = st;
+        used = true;
+    }
+};
+
+// Per-device context for the calls that take a device ordinal rather than an
+// index (merge, select): persistent scratch, its own stream, stream ordering.
+// Never destroyed (process lifetime): freeing at static destruction would race
+// with the CUDA runtime's own teardown.
+struct DeviceCtx {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    StreamOrder order;
+    DevBuf tmp, cnt, scr, io;
+};
+DeviceCtx& device_ctx(int device) {
+    static std::mutex mu;
+    static std::array<DeviceCtx*, kMaxDevices> ctx{};
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ctx[device]) {
+        DeviceGuard dg(device);
+        auto* c = new DeviceCtx();
+        RBE_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        RBE_CK(cudaEventCreateWithFlags(&c->order.done, cudaEventDisableTiming));
+        ctx[device] = c;
+    }
+    return *ctx[device];
+}
+
+__global__ void gather_lists_kernel(const Result* in, uint32_t n_lists, uint32_t Q, uint64_t n, Result* out,
+                                    unsigned long long* counts) {
+    const uint64_t total = uint64_t(n_lists) * Q * n;
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
+        const Result r = in[e];
+        if (!r.valid) continue;
+        const uint32_t q = uint32_t((e / n) % Q);
+        const unsigned long long pos = atomicAdd(counts + q, 1ull);
+        out[uint64_t(q) * n_lists * n + pos] = r;
+    }
+}
+
+// Enqueue the merge of n_lists result lists per query (in = [n_lists][Q][n]) into
+// out = [Q][n] on stream st, with the scratch buffers given (no host synchronisation).
+void enqueue_merge(const Result* d_in, uint32_t n_lists, uint32_t Q, uint64_t n, Result* d_out, DevBuf& tmp,
+                   DevBuf& cnt, DevBuf& scr, cudaStream_t st) {
+    const uint64_t cap = uint64_t(n_lists) * n;
+    tmp.ensure(sizeof(Result) * cap * Q);
+    cnt.ensure(sizeof(unsigned long long) * Q);
+    RBE_CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * Q, st));
+    const uint64_t total = cap * Q;
+    gather_lists_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 65535)), 256, 0, st>>>(
+        d_in, n_lists, Q, n, tmp.as<Result>(), cnt.as<unsigned long long>());
+    RBE_CK(cudaGetLastError());
+    const size_t ss = select_scratch_bytes(Q, cap, n);
+    scr.ensure(ss);
+    launch_select_topn(tmp.as<Result>(), cnt.as<unsigned long long>(), cap, Q, n, d_out, scr.p, ss, st);
+}
+
 }  // namespace
 
 struct rbe_cuda_index {
@@ -99,38 +223,40 @@ struct rbe_cuda_index {
         uint64_t* ids;
     };
     std::vector<Local> parts;
-    void* store = nullptr;
-    size_t store_bytes = 0;
-    PartDesc* d_parts = nullptr;
+    uint64_t total = 0;  // documents held by this handle
+    DevBuf store;
+    DevBuf d_parts;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[4] = {};
+    cudaEvent_t ev[4] = {};  // batch start, scan start, scan end, batch end (timing)
+    StreamOrder order;       // scratch ownership across streams
     std::mutex mu;
     // per-batch scratch, grown on demand
     DevBuf queries, qperm, qtensor, surv, surv_count, counters, queue_scratch, sel_scratch, out, probe, thresholds, soa;
+    // multi-handle search, on the root handle: the gathered lists, the merged list, merge scratch
+    DevBuf gathered, merged, mtmp, mcnt, mscr;
+    DevBuf sticky;               // u32 internal-consistency flag, cleared only when reported
     bool mag_range_ok = false;   // cached magnitude range (tensor threshold bins)
     float mag_lo = 0.0f, mag_hi = 0.0f;
-    Result* host_out = nullptr;  // pinned staging for the D2H of results
+    uint8_t* host_out = nullptr;  // page-locked staging for result D2H (+ flags)
     size_t host_out_cap = 0;
-    void ensure_host_out(size_t n) {
-        if (n <= host_out_cap) return;
+    void ensure_host_out(size_t bytes) {
+        if (bytes <= host_out_cap) return;
         if (host_out) cudaFreeHost(host_out);
         host_out = nullptr;
         host_out_cap = 0;
-        RBE_CK(cudaMallocHost(&host_out, n * sizeof(Result)));
-        host_out_cap = n;
+        RBE_CK(cudaMallocHost(&host_out, bytes));
+        host_out_cap = bytes;
     }
 
     ~rbe_cuda_index() {
         cudaSetDevice(device);
-        for (DevBuf* b : {&queries, &qperm, &qtensor, &surv, &surv_count, &counters, &queue_scratch, &sel_scratch, &out,
-                          &probe, &thresholds, &soa})
-            b->release();
-        if (d_parts) cudaFree(d_parts);
-        if (store) cudaFree(store);
+        if (stream) cudaStreamSynchronize(stream);
         if (host_out) cudaFreeHost(host_out);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        if (order.done) cudaEventDestroy(order.done);
         if (stream) cudaStreamDestroy(stream);
+        // DevBuf members free themselves (device already current)
     }
 };
 
@@ -147,25 +273,9 @@ bool pinned_host(const void* p) {
     return at.type == cudaMemoryTypeHost;
 }
 
-void check_device_usable(int device) {
-    int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess || n == 0)
-        throw CudaError(std::string("no usable CUDA device (") + cudaGetErrorString(e) +
-                        "); the RBE search path has no CPU fallback");
-    if (device < 0 || device >= n) throw InvalidArgument("rbe_cuda: device ordinal out of range");
-    cudaDeviceProp prop;
-    RBE_CK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10)
-        throw CudaError("rbe_cuda: kernels are compiled for sm_100a (B200); device " + std::to_string(device) +
-                        " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
-}
-
-// Reference-order argument checks of search / local_select (search.cpp:62-71, 80-82, 133-135).
-void validate_search(const rbe_cuda_index* ix, uint32_t qp, const rbe_scan_geometry* g) {
-    uint64_t total = 0;
-    for (auto& p : ix->parts) total += p.count;
-    if (ix->parts.empty() || total == 0) throw InvalidArgument("search: empty index");
+// Reference-order argument checks of local_select (search.cpp:62-71, 80-82) for one handle;
+// the empty-index check of search (search.cpp:133-135) is done over all handles by the caller.
+void validate_shape(const rbe_cuda_index* ix, uint32_t qp, const rbe_scan_geometry* g) {
     if (qp == 0) throw InvalidArgument("local_select: query dimension mismatch");
     if (g->queue_length == 0) throw InvalidArgument("local_select: queue_length must be positive");
     const uint64_t capacity = uint64_t(g->blocks) * g->threads_per_block * g->items_per_thread;
@@ -173,20 +283,41 @@ void validate_search(const rbe_cuda_index* ix, uint32_t qp, const rbe_scan_geome
         if (capacity < p.count) throw InvalidArgument("local_select: geometry does not cover partition");
     if (uint64_t(qp) * ix->shape.kp > 64) throw InvalidArgument("local_select: too many planes");
 }
+void validate_search(const rbe_cuda_index* ix, uint32_t qp, const rbe_scan_geometry* g) {
+    if (ix->parts.empty() || ix->total == 0) throw InvalidArgument("search: empty index");
+    validate_shape(ix, qp, g);
+}
 
-struct BatchResult {
+// Reports (and clears) the sticky internal-consistency flag; `flag` is its value as read
+// back by the caller's synchronous copy.
+void report_sticky(rbe_cuda_index* ix, uint32_t flag) {
+    if (!flag) return;
+    RBE_CK(cudaMemsetAsync(ix->sticky.p, 0, 4, ix->stream));
+    RBE_CK(cudaStreamSynchronize(ix->stream));
+    throw std::logic_error("tensor scan: accumulator recovery failed (internal error)");
+}
+void check_sticky_sync(rbe_cuda_index* ix, cudaStream_t st) {
+    uint32_t* h = reinterpret_cast<uint32_t*>(ix->host_out);
+    RBE_CK(cudaMemcpyAsync(h, ix->sticky.p, 4, cudaMemcpyDeviceToHost, st));
+    RBE_CK(cudaStreamSynchronize(st));
+    report_sticky(ix, *h);
+}
+
+struct Pending {
     rbe_search_stats stats{};
+    uint64_t surv_cap = 0;
+    uint32_t Q = 0;
 };
 
-// Runs one batch with queries already on the device (ix->queries) and leaves
-// rbe_result[Q][n] in ix->out.  Returns stats.
-// sync = false (tensor variant only): the whole batch is enqueued on `st` with no host
-// synchronisation (no stats; the consistency flag is checked by the next synchronous call).
-void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, const rbe_scan_geometry* g, uint64_t n,
-               const rbe_search_options* opt, rbe_search_stats* st_out, bool sync = true) {
+// Enqueue one batch with the queries already on the device (ix->queries); leaves
+// rbe_result[Q][n] in ix->out.  The tensor variant never synchronises here; the
+// exact variant does (its survivor-overflow retry).  The caller holds ix->mu, has
+// acquired ix->order on st and releases it afterwards.
+Pending enqueue_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, const rbe_scan_geometry* g,
+                      uint64_t n, const rbe_search_options* opt) {
     const Shape& s = ix->shape;
     ScanArgs a;
-    a.parts = ix->d_parts;
+    a.parts = ix->d_parts.as<PartDesc>();
     a.n_parts = uint32_t(ix->parts.size());
     a.blocks = g->blocks;
     a.tpb = g->threads_per_block;
@@ -202,25 +333,24 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
     if (variant == RBE_VARIANT_TENSOR && !tensor_ok)
         throw InvalidArgument("search: tensor variant unsupported for this shape: " + why);
     if (variant == RBE_VARIANT_AUTO) variant = tensor_ok ? RBE_VARIANT_TENSOR : RBE_VARIANT_EXACT;
-    if (variant != RBE_VARIANT_TENSOR) sync = true;  // the exact kernel may need its overflow retry
 
-    rbe_search_stats stats{};
-    stats.variant = variant;
+    Pending pd;
+    pd.Q = Q;
+    pd.stats.variant = variant;
     ix->counters.ensure(64);
     unsigned long long* d_scored = ix->counters.as<unsigned long long>();
     unsigned int* d_overflow = reinterpret_cast<unsigned int*>(d_scored + 2);
-    unsigned int* d_error = d_overflow + 1;
     unsigned long long* d_cands = d_scored + 4;
     a.scored = d_scored;
     a.overflow = d_overflow;
-    a.error = d_error;
+    a.error = ix->sticky.as<unsigned int>();
     if (variant == RBE_VARIANT_TENSOR && !ix->mag_range_ok) {
         // one-time (per index contents) magnitude range for the threshold bins
         uint32_t* d_rng = reinterpret_cast<uint32_t*>(d_scored + 6);
         const uint32_t init[2] = {0xffffffffu, 0u};
         RBE_CK(cudaMemcpyAsync(d_rng, init, 8, cudaMemcpyHostToDevice, st));
         for (auto& p : ix->parts) launch_mag_range(p.mags, p.count, d_rng, st);
-        uint32_t rng[2];
+        uint32_t* rng = reinterpret_cast<uint32_t*>(ix->host_out);
         RBE_CK(cudaMemcpyAsync(rng, d_rng, 8, cudaMemcpyDeviceToHost, st));
         RBE_CK(cudaStreamSynchronize(st));
         std::memcpy(&ix->mag_lo, &rng[0], 4);
@@ -251,72 +381,121 @@ void run_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, con
             RBE_CK(cudaEventRecord(ix->ev[1], st));
             launch_scan_exact(a, s, ix->qperm.as<uint32_t>(), qs ? ix->queue_scratch.p : nullptr, st);
             RBE_CK(cudaEventRecord(ix->ev[2], st));
-            stats.launches += 2;
-        } else {
-            std::vector<uint64_t> counts;
-            for (auto& p : ix->parts) counts.push_back(p.count);
-            TensorScanPlan plan = plan_tensor_scan(s, qp, *g, Q, counts, n, probe_tiles);
-            a.surv_cap = plan.surv_cap;
-            ix->surv.ensure(sizeof(Result) * a.surv_cap * Q);
-            a.surv = ix->surv.as<Result>();
-            ix->qtensor.ensure(plan.query_bytes);
-            ix->probe.ensure(plan.probe_bytes);
-            ix->thresholds.ensure(plan.threshold_bytes);
-            ix->queue_scratch.ensure(plan.state_bytes);
-            RBE_CK(cudaEventRecord(ix->ev[1], st));
-            stats.launches += run_tensor_scan(plan, a, s, ix->queries.as<uint64_t>(), ix->qtensor.p, ix->probe.p,
-                                              ix->thresholds.p, ix->queue_scratch.p, d_cands, st);
-            RBE_CK(cudaEventRecord(ix->ev[2], st));
+            pd.stats.launches += 2;
+            // survivor-list overflow cannot happen by construction (cap = every per-thread
+            // survivor); checked anyway, synchronously
+            uint32_t* h = reinterpret_cast<uint32_t*>(ix->host_out);
+            RBE_CK(cudaMemcpyAsync(h, d_overflow, 4, cudaMemcpyDeviceToHost, st));
+            RBE_CK(cudaStreamSynchronize(st));
+            if (*h) throw std::logic_error("exact scan overflowed its survivor list");
+            break;
         }
-        if (!sync) break;  // the tensor kernel never sets the overflow flag
-        unsigned int flags[2] = {0, 0};
-        RBE_CK(cudaMemcpyAsync(flags, d_overflow, sizeof(flags), cudaMemcpyDeviceToHost, st));
-        RBE_CK(cudaStreamSynchronize(st));
-        if (flags[1]) throw std::logic_error("tensor scan: accumulator recovery failed (internal error)");
-        const unsigned int overflow = flags[0];
-        if (!overflow) break;
-        if (variant == RBE_VARIANT_EXACT) throw std::logic_error("exact scan overflowed its survivor list");
-        // candidate/survivor buffer overflow in the tensor kernel: redo exactly.
-        variant = RBE_VARIANT_EXACT;
-        stats.variant = variant;
-        stats.fallback = 1;
+        std::vector<uint64_t> counts;
+        for (auto& p : ix->parts) counts.push_back(p.count);
+        TensorScanPlan plan = plan_tensor_scan(s, qp, *g, Q, counts, n, probe_tiles);
+        a.surv_cap = plan.surv_cap;
+        ix->surv.ensure(sizeof(Result) * a.surv_cap * Q);
+        a.surv = ix->surv.as<Result>();
+        ix->qtensor.ensure(plan.query_bytes);
+        ix->probe.ensure(plan.probe_bytes);
+        ix->thresholds.ensure(plan.threshold_bytes);
+        ix->queue_scratch.ensure(plan.state_bytes);
+        RBE_CK(cudaEventRecord(ix->ev[1], st));
+        pd.stats.launches += run_tensor_scan(plan, a, s, ix->queries.as<uint64_t>(), ix->qtensor.p, ix->probe.p,
+                                             ix->thresholds.p, ix->queue_scratch.p, d_cands, st);
+        RBE_CK(cudaEventRecord(ix->ev[2], st));
+        break;  // the tensor kernel emits at most one survivor per logical thread: never overflows
     }
     const size_t ss = select_scratch_bytes(Q, a.surv_cap, n);
     ix->sel_scratch.ensure(ss);
     ix->out.ensure(sizeof(Result) * size_t(Q) * n);
     launch_select_topn(a.surv, a.surv_count, a.surv_cap, Q, n, ix->out.as<Result>(), ix->sel_scratch.p, ss, st);
-    stats.launches += 1;
+    pd.stats.launches += 1;
     RBE_CK(cudaEventRecord(ix->ev[3], st));
-    if (!sync) {
-        if (st_out) *st_out = stats;
-        return;
-    }
-    unsigned long long host_counters[8];
-    RBE_CK(cudaMemcpyAsync(host_counters, ix->counters.p, 64, cudaMemcpyDeviceToHost, st));
-    std::vector<unsigned long long> sc(Q);
-    RBE_CK(cudaMemcpyAsync(sc.data(), ix->surv_count.p, sizeof(unsigned long long) * Q, cudaMemcpyDeviceToHost, st));
+    pd.surv_cap = a.surv_cap;
+    return pd;
+}
+
+// Wait for an enqueued batch, read its counters and the sticky flag (reported as an
+// error), and fill the stats.
+void finish_batch(rbe_cuda_index* ix, cudaStream_t st, const Pending& pd, rbe_search_stats* st_out) {
+    const uint32_t Q = pd.Q;
+    ix->ensure_host_out(64 + 8 + sizeof(unsigned long long) * Q);
+    unsigned long long* hc = reinterpret_cast<unsigned long long*>(ix->host_out);
+    uint32_t* hflag = reinterpret_cast<uint32_t*>(hc + 8);
+    unsigned long long* hs = hc + 9;
+    RBE_CK(cudaMemcpyAsync(hc, ix->counters.p, 64, cudaMemcpyDeviceToHost, st));
+    RBE_CK(cudaMemcpyAsync(hflag, ix->sticky.p, 4, cudaMemcpyDeviceToHost, st));
+    RBE_CK(cudaMemcpyAsync(hs, ix->surv_count.p, sizeof(unsigned long long) * Q, cudaMemcpyDeviceToHost, st));
     RBE_CK(cudaStreamSynchronize(st));
-    stats.scored = host_counters[0];
-    stats.candidates = host_counters[4];
-    for (auto c : sc) stats.survivors += std::min<uint64_t>(c, a.surv_cap);
+    report_sticky(ix, *hflag);
+    if (!st_out) return;
+    rbe_search_stats stats = pd.stats;
+    stats.scored = hc[0];
+    stats.candidates = hc[4];
+    for (uint32_t q = 0; q < Q; ++q) stats.survivors += std::min<uint64_t>(hs[q], pd.surv_cap);
     float ms = 0;
     RBE_CK(cudaEventElapsedTime(&ms, ix->ev[1], ix->ev[2]));
     stats.scan_ms = ms;
     RBE_CK(cudaEventElapsedTime(&ms, ix->ev[0], ix->ev[3]));
     stats.total_ms = ms;
-    if (st_out) *st_out = stats;
+    *st_out = stats;
 }
 
-__global__ void gather_lists_kernel(const Result* in, uint32_t n_lists, uint32_t Q, uint64_t n, Result* out,
-                                    unsigned long long* counts) {
-    const uint64_t total = uint64_t(n_lists) * Q * n;
-    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-        const Result r = in[e];
-        if (!r.valid) continue;
-        const uint32_t q = uint32_t((e / n) % Q);
-        const unsigned long long pos = atomicAdd(counts + q, 1ull);
-        out[uint64_t(q) * n_lists * n + pos] = r;
+struct HostOut {
+    double* scores;
+    uint64_t* ids;
+    uint32_t* partitions;
+    int64_t* accs;
+    uint64_t* counts;
+};
+
+// Device result records [Q][n] on ix's device -> the caller's host arrays (one
+// device-side conversion to their layout, then DMA straight into page-locked arrays
+// or one staged copy for pageable ones), the sticky flag read back with them.
+void deliver(rbe_cuda_index* ix, const Result* d_res, uint32_t Q, uint64_t n, const HostOut& o, cudaStream_t st) {
+    const size_t ne = size_t(Q) * n;
+    const size_t b8 = ne * 8, b4 = ne * 4;
+    ix->soa.ensure(3 * b8 + b4 + size_t(Q) * 8 + 256);
+    uint8_t* base = static_cast<uint8_t*>(ix->soa.p);
+    double* dS = reinterpret_cast<double*>(base);
+    uint64_t* dI = reinterpret_cast<uint64_t*>(base + b8);
+    int64_t* dA = reinterpret_cast<int64_t*>(base + 2 * b8);
+    uint64_t* dC = reinterpret_cast<uint64_t*>(base + 3 * b8);
+    uint32_t* dP = reinterpret_cast<uint32_t*>(base + 3 * b8 + size_t(Q) * 8);
+    launch_results_to_soa(d_res, Q, n, dS, dI, dP, o.accs ? dA : nullptr, dC, st);
+    const bool pinned = pinned_host(o.scores) && pinned_host(o.ids) && pinned_host(o.partitions) &&
+                        pinned_host(o.counts) && (!o.accs || pinned_host(o.accs));
+    const size_t total = 3 * b8 + b4 + size_t(Q) * 8;
+    ix->ensure_host_out(16 + (pinned ? 0 : total));
+    uint32_t* hflag = reinterpret_cast<uint32_t*>(ix->host_out);
+    uint8_t* h = ix->host_out + 16;
+    if (pinned) {
+        RBE_CK(cudaMemcpyAsync(o.scores, dS, b8, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaMemcpyAsync(o.ids, dI, b8, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaMemcpyAsync(o.partitions, dP, b4, cudaMemcpyDeviceToHost, st));
+        if (o.accs) RBE_CK(cudaMemcpyAsync(o.accs, dA, b8, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaMemcpyAsync(o.counts, dC, size_t(Q) * 8, cudaMemcpyDeviceToHost, st));
+    } else {
+        RBE_CK(cudaMemcpyAsync(h, base, total, cudaMemcpyDeviceToHost, st));
     }
+    RBE_CK(cudaMemcpyAsync(hflag, ix->sticky.p, 4, cudaMemcpyDeviceToHost, st));
+    RBE_CK(cudaStreamSynchronize(st));
+    report_sticky(ix, *hflag);
+    if (!pinned) {
+        std::memcpy(o.scores, h, b8);
+        std::memcpy(o.ids, h + b8, b8);
+        if (o.accs) std::memcpy(o.accs, h + 2 * b8, b8);
+        std::memcpy(o.counts, h + 3 * b8, size_t(Q) * 8);
+        std::memcpy(o.partitions, h + 3 * b8 + size_t(Q) * 8, b4);
+    }
+}
+
+void rethrow_status(int rc) {
+    if (rc == RBE_CUDA_OK) return;
+    if (rc == RBE_CUDA_EINVAL) throw InvalidArgument(g_last_error);
+    if (rc == RBE_CUDA_ERANGE) throw OutOfRange(g_last_error);
+    throw CudaError(g_last_error);
 }
 
 }  // namespace
@@ -325,7 +504,7 @@ extern "C" {
 
 const char* rbe_cuda_last_error(void) { return g_last_error.c_str(); }
 
-const char* rbe_cuda_version(void) { return "rbe_cuda 0.1 sm_100a"; }
+const char* rbe_cuda_version(void) { return "rbe_cuda 0.2 sm_100a"; }
 
 int rbe_cuda_index_create(const rbe_index_shape* shape, uint32_t n_partitions, const uint32_t* ordinals,
                           const uint64_t* counts, int device, rbe_cuda_index** out) {
@@ -354,17 +533,20 @@ int rbe_cuda_index_create(const rbe_index_shape* shape, uint32_t n_partitions, c
             off += round_up(cp * 4, 256);
             off += round_up(std::max<uint64_t>(counts[i], 1) * 8, 256);
         }
-        ix->store_bytes = off;
-        if (off) RBE_CK(cudaMalloc(&ix->store, off));
-        std::vector<PartDesc> descs;
+        ix->store.ensure(off);
         RBE_CK(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
         for (auto& e : ix->ev) RBE_CK(cudaEventCreate(&e));
+        RBE_CK(cudaEventCreateWithFlags(&ix->order.done, cudaEventDisableTiming));
+        ix->ensure_host_out(4096);
+        ix->sticky.ensure(4);
+        RBE_CK(cudaMemsetAsync(ix->sticky.p, 0, 4, ix->stream));
+        std::vector<PartDesc> descs;
         for (uint32_t i = 0; i < n_partitions; ++i) {
             rbe_cuda_index::Local L;
             L.ordinal = ordinals[i];
             L.count = counts[i];
             L.count_pad = round_up(counts[i], 512) + 512;
-            char* base = static_cast<char*>(ix->store) + offs[i];
+            char* base = static_cast<char*>(ix->store.p) + offs[i];
             L.planes = reinterpret_cast<uint32_t*>(base);
             base += round_up(size_t(ix->shape.kp) * L.count_pad * ix->shape.w32 * 4, 256);
             L.mags = reinterpret_cast<float*>(base);
@@ -373,12 +555,13 @@ int rbe_cuda_index_create(const rbe_index_shape* shape, uint32_t n_partitions, c
             RBE_CK(cudaMemsetAsync(L.planes, 0, size_t(ix->shape.kp) * L.count_pad * ix->shape.w32 * 4, ix->stream));
             launch_fill_f32(L.mags, L.count_pad, 1.0f, ix->stream);
             ix->parts.push_back(L);
+            ix->total += L.count;
             PartDesc d{L.planes, L.mags, L.ids, L.count, L.count_pad, L.ordinal, 0};
             descs.push_back(d);
         }
         if (!descs.empty()) {
-            RBE_CK(cudaMalloc(&ix->d_parts, sizeof(PartDesc) * descs.size()));
-            RBE_CK(cudaMemcpyAsync(ix->d_parts, descs.data(), sizeof(PartDesc) * descs.size(), cudaMemcpyHostToDevice,
+            ix->d_parts.ensure(sizeof(PartDesc) * descs.size());
+            RBE_CK(cudaMemcpyAsync(ix->d_parts.p, descs.data(), sizeof(PartDesc) * descs.size(), cudaMemcpyHostToDevice,
                                    ix->stream));
         }
         RBE_CK(cudaStreamSynchronize(ix->stream));
@@ -397,22 +580,24 @@ int rbe_cuda_index_upload_partition(rbe_cuda_index* ix, uint32_t i, const uint64
         if (L.count == 0) return;
         if (!planes || !mags || !ids) throw InvalidArgument("rbe_cuda_index_upload_partition: null buffer");
         const Shape& s = ix->shape;
+        cudaStream_t st = ix->stream;
+        ix->order.acquire(st);
         const size_t nat_bytes = size_t(s.kp) * L.count * s.wpp * 8;
         DevBuf tmp;
         tmp.ensure(nat_bytes + 64);
-        RBE_CK(cudaMemcpyAsync(tmp.p, planes, nat_bytes, cudaMemcpyHostToDevice, ix->stream));
-        launch_repack_planes(tmp.as<uint64_t>(), L.planes, L.count, L.count_pad, s, ix->perm, ix->stream);
+        RBE_CK(cudaMemcpyAsync(tmp.p, planes, nat_bytes, cudaMemcpyHostToDevice, st));
+        launch_repack_planes(tmp.as<uint64_t>(), L.planes, L.count, L.count_pad, s, ix->perm, st);
         ix->mag_range_ok = false;
-        RBE_CK(cudaMemcpyAsync(L.mags, mags, L.count * 4, cudaMemcpyHostToDevice, ix->stream));
-        RBE_CK(cudaMemcpyAsync(L.ids, ids, L.count * 8, cudaMemcpyHostToDevice, ix->stream));
+        RBE_CK(cudaMemcpyAsync(L.mags, mags, L.count * 4, cudaMemcpyHostToDevice, st));
+        RBE_CK(cudaMemcpyAsync(L.ids, ids, L.count * 8, cudaMemcpyHostToDevice, st));
         ix->counters.ensure(64);
-        RBE_CK(cudaMemsetAsync(ix->counters.p, 0, 4, ix->stream));
-        launch_validate_mags(L.mags, L.count, ix->counters.as<uint32_t>(), ix->stream);
-        uint32_t bad = 0;
-        RBE_CK(cudaMemcpyAsync(&bad, ix->counters.p, 4, cudaMemcpyDeviceToHost, ix->stream));
-        RBE_CK(cudaStreamSynchronize(ix->stream));
-        tmp.release();
-        if (bad) throw InvalidArgument("rbe_cuda_index_upload_partition: keyword magnitudes must be finite and > 0");
+        RBE_CK(cudaMemsetAsync(ix->counters.p, 0, 4, st));
+        launch_validate_mags(L.mags, L.count, ix->counters.as<uint32_t>(), st);
+        uint32_t* bad = reinterpret_cast<uint32_t*>(ix->host_out);
+        RBE_CK(cudaMemcpyAsync(bad, ix->counters.p, 4, cudaMemcpyDeviceToHost, st));
+        ix->order.release(st);
+        RBE_CK(cudaStreamSynchronize(st));
+        if (*bad) throw InvalidArgument("rbe_cuda_index_upload_partition: keyword magnitudes must be finite and > 0");
     });
 }
 
@@ -422,6 +607,8 @@ int rbe_cuda_index_fill_synthetic(rbe_cuda_index* ix, uint64_t seed, uint64_t n_
         std::lock_guard<std::mutex> lk(ix->mu);
         DeviceGuard dg(ix->device);
         if (n_parts_total == 0) throw InvalidArgument("rbe_cuda_index_fill_synthetic: need at least one partition");
+        cudaStream_t st = ix->stream;
+        ix->order.acquire(st);
         ix->mag_range_ok = false;
         for (auto& L : ix->parts) {
             if (L.ordinal >= n_parts_total) throw InvalidArgument("rbe_cuda_index_fill_synthetic: ordinal >= partitions");
@@ -429,9 +616,10 @@ int rbe_cuda_index_fill_synthetic(rbe_cuda_index* ix, uint64_t seed, uint64_t n_
             if (expect != L.count)
                 throw InvalidArgument("rbe_cuda_index_fill_synthetic: partition count does not match round-robin split");
             launch_fill_synthetic(L.planes, L.mags, L.ids, L.count, L.count_pad, L.ordinal, n_parts_total, n_total, seed,
-                                  ix->shape, ix->perm, ix->stream);
+                                  ix->shape, ix->perm, st);
         }
-        RBE_CK(cudaStreamSynchronize(ix->stream));
+        ix->order.release(st);
+        RBE_CK(cudaStreamSynchronize(st));
     });
 }
 
@@ -446,14 +634,17 @@ int rbe_cuda_index_download_partition(const rbe_cuda_index* cix, uint32_t i, uin
         auto& L = ix->parts[i];
         if (L.count == 0) return;
         const Shape& s = ix->shape;
+        cudaStream_t st = ix->stream;
+        ix->order.acquire(st);
         const size_t nat_bytes = size_t(s.kp) * L.count * s.wpp * 8;
         DevBuf tmp;
         tmp.ensure(nat_bytes);
-        launch_unpack_planes(L.planes, tmp.as<uint64_t>(), L.count, L.count_pad, s, ix->perm, ix->stream);
-        if (planes) RBE_CK(cudaMemcpyAsync(planes, tmp.p, nat_bytes, cudaMemcpyDeviceToHost, ix->stream));
-        if (mags) RBE_CK(cudaMemcpyAsync(mags, L.mags, L.count * 4, cudaMemcpyDeviceToHost, ix->stream));
-        if (ids) RBE_CK(cudaMemcpyAsync(ids, L.ids, L.count * 8, cudaMemcpyDeviceToHost, ix->stream));
-        RBE_CK(cudaStreamSynchronize(ix->stream));
+        launch_unpack_planes(L.planes, tmp.as<uint64_t>(), L.count, L.count_pad, s, ix->perm, st);
+        if (planes) RBE_CK(cudaMemcpyAsync(planes, tmp.p, nat_bytes, cudaMemcpyDeviceToHost, st));
+        if (mags) RBE_CK(cudaMemcpyAsync(mags, L.mags, L.count * 4, cudaMemcpyDeviceToHost, st));
+        if (ids) RBE_CK(cudaMemcpyAsync(ids, L.ids, L.count * 8, cudaMemcpyDeviceToHost, st));
+        ix->order.release(st);
+        RBE_CK(cudaStreamSynchronize(st));
     });
 }
 
@@ -464,10 +655,8 @@ int rbe_cuda_index_destroy(rbe_cuda_index* ix) {
 int rbe_cuda_index_bytes(const rbe_cuda_index* ix, uint64_t* device_bytes, uint64_t* scan_bytes) {
     return guarded([&] {
         if (!ix) throw InvalidArgument("rbe_cuda_index_bytes: null index");
-        uint64_t docs = 0;
-        for (auto& L : ix->parts) docs += L.count;
-        if (device_bytes) *device_bytes = ix->store_bytes;
-        if (scan_bytes) *scan_bytes = docs * (uint64_t(ix->shape.kp) * ix->shape.wpp * 8 + 4);
+        if (device_bytes) *device_bytes = ix->store.bytes;
+        if (scan_bytes) *scan_bytes = ix->total * (uint64_t(ix->shape.kp) * ix->shape.wpp * 8 + 4);
     });
 }
 
@@ -484,12 +673,14 @@ int rbe_cuda_search_device(rbe_cuda_index* ix, const uint64_t* d_query_words, ui
         // all work is issued on the caller's stream when given (so its events
         // bracket exactly this batch), else on the index's own stream
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ix->stream;
+        ix->order.acquire(st);
         const size_t qbytes = size_t(n_queries) * query_planes * ix->shape.wpp * 8;
         ix->queries.ensure(qbytes);
         RBE_CK(cudaMemcpyAsync(ix->queries.p, d_query_words, qbytes, cudaMemcpyDeviceToDevice, st));
-        run_batch(ix, st, n_queries, query_planes, geometry, n, options, stats, stats != nullptr);
+        const Pending pd = enqueue_batch(ix, st, n_queries, query_planes, geometry, n, options);
         RBE_CK(cudaMemcpyAsync(d_out, ix->out.p, sizeof(Result) * n_queries * n, cudaMemcpyDeviceToDevice, st));
-        if (stats) RBE_CK(cudaStreamSynchronize(st));
+        ix->order.release(st);
+        if (stats) finish_batch(ix, st, pd, stats);
     });
 }
 
@@ -509,54 +700,16 @@ int rbe_cuda_search(rbe_cuda_index* ix, const uint64_t* query_words, uint32_t n_
         }
         if (!query_words || !scores || !ids || !partitions || !counts)
             throw InvalidArgument("rbe_cuda_search: null buffer");
+        cudaStream_t st = ix->stream;
+        ix->order.acquire(st);
         const size_t qbytes = size_t(n_queries) * query_planes * ix->shape.wpp * 8;
         ix->queries.ensure(qbytes);
-        RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, ix->stream));
-        // without stats the batch runs with a single host synchronisation (after the D2H below)
-        run_batch(ix, ix->stream, n_queries, query_planes, geometry, n, options, stats, stats != nullptr);
-        const size_t ne = size_t(n_queries) * n;
-        if (pinned_host(scores) && pinned_host(ids) && pinned_host(partitions) && pinned_host(counts) &&
-            (!accs || pinned_host(accs))) {
-            // caller buffers in pinned host memory: convert to their layout on the device and DMA
-            // straight into them (no staging, no host scatter)
-            const size_t b8 = ne * 8, b4 = ne * 4;
-            ix->soa.ensure(3 * b8 + b4 + size_t(n_queries) * 8 + 256);
-            uint8_t* base = static_cast<uint8_t*>(ix->soa.p);
-            double* dS = reinterpret_cast<double*>(base);
-            uint64_t* dI = reinterpret_cast<uint64_t*>(base + b8);
-            int64_t* dA = reinterpret_cast<int64_t*>(base + 2 * b8);
-            uint64_t* dC = reinterpret_cast<uint64_t*>(base + 3 * b8);
-            uint32_t* dP = reinterpret_cast<uint32_t*>(base + 3 * b8 + size_t(n_queries) * 8);
-            launch_results_to_soa(ix->out.as<Result>(), n_queries, n, dS, dI, dP, accs ? dA : nullptr, dC, ix->stream);
-            RBE_CK(cudaMemcpyAsync(scores, dS, b8, cudaMemcpyDeviceToHost, ix->stream));
-            RBE_CK(cudaMemcpyAsync(ids, dI, b8, cudaMemcpyDeviceToHost, ix->stream));
-            RBE_CK(cudaMemcpyAsync(partitions, dP, b4, cudaMemcpyDeviceToHost, ix->stream));
-            if (accs) RBE_CK(cudaMemcpyAsync(accs, dA, b8, cudaMemcpyDeviceToHost, ix->stream));
-            RBE_CK(cudaMemcpyAsync(counts, dC, size_t(n_queries) * 8, cudaMemcpyDeviceToHost, ix->stream));
-            RBE_CK(cudaStreamSynchronize(ix->stream));
-            return;
-        }
-        // pageable caller buffers: the same device-side conversion, one D2H into pinned staging,
-        // then contiguous copies (no per-record scatter on the host)
-        const size_t b8 = ne * 8, b4 = ne * 4;
-        ix->soa.ensure(3 * b8 + b4 + size_t(n_queries) * 8 + 256);
-        uint8_t* base = static_cast<uint8_t*>(ix->soa.p);
-        double* dS = reinterpret_cast<double*>(base);
-        uint64_t* dI = reinterpret_cast<uint64_t*>(base + b8);
-        int64_t* dA = reinterpret_cast<int64_t*>(base + 2 * b8);
-        uint64_t* dC = reinterpret_cast<uint64_t*>(base + 3 * b8);
-        uint32_t* dP = reinterpret_cast<uint32_t*>(base + 3 * b8 + size_t(n_queries) * 8);
-        launch_results_to_soa(ix->out.as<Result>(), n_queries, n, dS, dI, dP, accs ? dA : nullptr, dC, ix->stream);
-        const size_t total = 3 * b8 + b4 + size_t(n_queries) * 8;
-        ix->ensure_host_out((total + sizeof(Result) - 1) / sizeof(Result));
-        uint8_t* h = reinterpret_cast<uint8_t*>(ix->host_out);
-        RBE_CK(cudaMemcpyAsync(h, base, total, cudaMemcpyDeviceToHost, ix->stream));
-        RBE_CK(cudaStreamSynchronize(ix->stream));
-        std::memcpy(scores, h, b8);
-        std::memcpy(ids, h + b8, b8);
-        if (accs) std::memcpy(accs, h + 2 * b8, b8);
-        std::memcpy(counts, h + 3 * b8, size_t(n_queries) * 8);
-        std::memcpy(partitions, h + 3 * b8 + size_t(n_queries) * 8, b4);
+        RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, st));
+        const Pending pd = enqueue_batch(ix, st, n_queries, query_planes, geometry, n, options);
+        // without stats the batch runs with a single host synchronisation (inside deliver)
+        deliver(ix, ix->out.as<Result>(), n_queries, n, HostOut{scores, ids, partitions, accs, counts}, st);
+        ix->order.release(st);
+        if (stats) finish_batch(ix, st, pd, stats);
     });
 }
 
@@ -581,6 +734,8 @@ int rbe_cuda_index_last_batch_ms(rbe_cuda_index* ix, double* scan_ms, double* to
         std::lock_guard<std::mutex> lk(ix->mu);
         DeviceGuard dg(ix->device);
         RBE_CK(cudaEventSynchronize(ix->ev[3]));
+        // surface an accumulator-recovery failure of any batch enqueued without stats
+        check_sticky_sync(ix, ix->stream);
         float ms = 0;
         RBE_CK(cudaEventElapsedTime(&ms, ix->ev[1], ix->ev[2]));
         if (scan_ms) *scan_ms = ms;
@@ -589,29 +744,140 @@ int rbe_cuda_index_last_batch_ms(rbe_cuda_index* ix, double* scan_ms, double* to
     });
 }
 
+int rbe_cuda_index_check(rbe_cuda_index* ix) {
+    return guarded([&] {
+        if (!ix) throw InvalidArgument("rbe_cuda_index_check: null index");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        DeviceGuard dg(ix->device);
+        if (ix->order.used) RBE_CK(cudaEventSynchronize(ix->order.done));
+        check_sticky_sync(ix, ix->stream);
+    });
+}
+
+int rbe_cuda_index_inject_error(rbe_cuda_index* ix) {
+    return guarded([&] {
+        if (!ix) throw InvalidArgument("rbe_cuda_index_inject_error: null index");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        DeviceGuard dg(ix->device);
+        const uint32_t one = 1;
+        RBE_CK(cudaMemcpyAsync(ix->sticky.p, &one, 4, cudaMemcpyHostToDevice, ix->stream));
+        RBE_CK(cudaStreamSynchronize(ix->stream));
+    });
+}
+
 int rbe_cuda_merge_device(int device, const rbe_result* d_in, uint32_t n_lists, uint32_t n_queries, uint64_t n,
                           rbe_result* d_out, void* stream) {
     return guarded([&] {
         check_device_usable(device);
-        DeviceGuard dg(device);
         if (n_queries == 0 || n == 0) return;
         if (!d_in || !d_out) throw InvalidArgument("rbe_cuda_merge_device: null buffer");
-        cudaStream_t st = static_cast<cudaStream_t>(stream);
-        const uint64_t cap = uint64_t(n_lists) * n;
-        DevBuf tmp, cnt, scr;
-        tmp.ensure(sizeof(Result) * cap * n_queries);
-        cnt.ensure(sizeof(unsigned long long) * n_queries);
-        RBE_CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * n_queries, st));
-        const uint64_t total = cap * n_queries;
-        gather_lists_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 65535)), 256, 0, st>>>(
-            reinterpret_cast<const Result*>(d_in), n_lists, n_queries, n, tmp.as<Result>(),
-            cnt.as<unsigned long long>());
-        RBE_CK(cudaGetLastError());
-        const size_t ss = select_scratch_bytes(n_queries, cap, n);
-        scr.ensure(ss);
-        launch_select_topn(tmp.as<Result>(), cnt.as<unsigned long long>(), cap, n_queries, n,
-                           reinterpret_cast<Result*>(d_out), scr.p, ss, st);
+        if (n_lists == 0) throw InvalidArgument("rbe_cuda_merge_device: need at least one list");
+        DeviceCtx& c = device_ctx(device);
+        std::lock_guard<std::mutex> lk(c.mu);
+        DeviceGuard dg(device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c.stream;
+        c.order.acquire(st);
+        enqueue_merge(reinterpret_cast<const Result*>(d_in), n_lists, n_queries, n, reinterpret_cast<Result*>(d_out),
+                      c.tmp, c.cnt, c.scr, st);
+        c.order.release(st);
+    });
+}
+
+int rbe_cuda_select_topn(int device, const double* scores, const uint64_t* ids, uint64_t count, uint32_t partition,
+                         uint64_t n, double* out_scores, uint64_t* out_ids, uint64_t* out_count) {
+    return guarded([&] {
+        check_device_usable(device);
+        if (!out_count) throw InvalidArgument("rbe_cuda_select_topn: null output");
+        *out_count = 0;
+        if (n == 0 || count == 0) return;
+        if (!scores || !ids || !out_scores || !out_ids) throw InvalidArgument("rbe_cuda_select_topn: null buffer");
+        DeviceCtx& c = device_ctx(device);
+        std::lock_guard<std::mutex> lk(c.mu);
+        DeviceGuard dg(device);
+        cudaStream_t st = c.stream;
+        c.order.acquire(st);
+        std::vector<Result> recs(count);
+        for (uint64_t i = 0; i < count; ++i) recs[i] = Result{scores[i], ids[i], 0, partition, 1u};
+        const uint64_t m = std::min<uint64_t>(n, count);
+        c.io.ensure(sizeof(Result) * (count + m) + sizeof(unsigned long long));
+        Result* d_in = c.io.as<Result>();
+        Result* d_out = d_in + count;
+        unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(d_out + m);
+        const unsigned long long cnt = count;
+        RBE_CK(cudaMemcpyAsync(d_in, recs.data(), sizeof(Result) * count, cudaMemcpyHostToDevice, st));
+        RBE_CK(cudaMemcpyAsync(d_cnt, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
+        const size_t ss = select_scratch_bytes(1, count, m);
+        c.scr.ensure(ss);
+        launch_select_topn(d_in, d_cnt, count, 1, m, d_out, c.scr.p, ss, st);
+        std::vector<Result> res(m);
+        RBE_CK(cudaMemcpyAsync(res.data(), d_out, sizeof(Result) * m, cudaMemcpyDeviceToHost, st));
+        c.order.release(st);
         RBE_CK(cudaStreamSynchronize(st));
+        uint64_t k = 0;
+        for (; k < m && res[k].valid; ++k) {
+            out_scores[k] = res[k].score;
+            out_ids[k] = res[k].id;
+        }
+        *out_count = k;
+    });
+}
+
+int rbe_cuda_local_select(rbe_cuda_index* ix, uint32_t i, const uint64_t* query_words, uint32_t query_planes,
+                          const rbe_scan_geometry* geometry, double* scores, uint64_t* slots, uint32_t* counts,
+                          uint64_t* scored) {
+    return guarded([&] {
+        if (!ix || !geometry) throw InvalidArgument("rbe_cuda_local_select: null argument");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        if (i >= ix->parts.size()) throw OutOfRange("rbe_cuda_local_select: partition out of range");
+        DeviceGuard dg(ix->device);
+        if (query_planes == 0) throw InvalidArgument("local_select: query dimension mismatch");
+        if (geometry->queue_length == 0) throw InvalidArgument("local_select: queue_length must be positive");
+        const auto& L = ix->parts[i];
+        if (uint64_t(geometry->blocks) * geometry->threads_per_block * geometry->items_per_thread < L.count)
+            throw InvalidArgument("local_select: geometry does not cover partition");
+        if (uint64_t(query_planes) * ix->shape.kp > 64) throw InvalidArgument("local_select: too many planes");
+        if (!query_words || !scores || !slots || !counts) throw InvalidArgument("rbe_cuda_local_select: null buffer");
+        const Shape& s = ix->shape;
+        cudaStream_t st = ix->stream;
+        ix->order.acquire(st);
+        ScanArgs a;
+        a.parts = ix->d_parts.as<PartDesc>() + i;
+        a.n_parts = 1;
+        a.blocks = geometry->blocks;
+        a.tpb = geometry->threads_per_block;
+        a.ipt = geometry->items_per_thread;
+        a.ql = geometry->queue_length;
+        a.Q = 1;
+        a.qp = query_planes;
+        const uint64_t threads = uint64_t(a.blocks) * a.tpb;
+        const uint64_t ql_eff = std::min<uint64_t>(a.ql, a.ipt);
+        const size_t qbytes = size_t(query_planes) * s.wpp * 8;
+        ix->queries.ensure(qbytes);
+        RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, st));
+        ix->counters.ensure(64);
+        RBE_CK(cudaMemsetAsync(ix->counters.p, 0, 64, st));
+        a.scored = ix->counters.as<unsigned long long>();
+        a.overflow = reinterpret_cast<unsigned int*>(a.scored + 2);
+        a.error = ix->sticky.as<unsigned int>();
+        const size_t lbytes = threads * ql_eff * 16 + threads * 4;
+        ix->surv.ensure(lbytes + 256);
+        a.list_scores = ix->surv.as<double>();
+        a.list_slots = reinterpret_cast<uint64_t*>(a.list_scores + threads * ql_eff);
+        a.list_counts = reinterpret_cast<uint32_t*>(a.list_slots + threads * ql_eff);
+        ix->qperm.ensure(sizeof(uint32_t) * size_t(s.kp) * query_planes * s.w32);
+        launch_prepare_queries_exact(ix->queries.as<uint64_t>(), ix->qperm.as<uint32_t>(), 1, query_planes, s, ix->perm,
+                                     st);
+        const size_t qs = exact_queue_scratch_bytes(a);
+        ix->queue_scratch.ensure(qs);
+        launch_scan_exact(a, s, ix->qperm.as<uint32_t>(), qs ? ix->queue_scratch.p : nullptr, st);
+        RBE_CK(cudaMemcpyAsync(scores, a.list_scores, threads * ql_eff * 8, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaMemcpyAsync(slots, a.list_slots, threads * ql_eff * 8, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaMemcpyAsync(counts, a.list_counts, threads * 4, cudaMemcpyDeviceToHost, st));
+        unsigned long long* hsc = reinterpret_cast<unsigned long long*>(ix->host_out);
+        RBE_CK(cudaMemcpyAsync(hsc, a.scored, 8, cudaMemcpyDeviceToHost, st));
+        ix->order.release(st);
+        RBE_CK(cudaStreamSynchronize(st));
+        if (scored) *scored = *hsc;
     });
 }
 
@@ -624,77 +890,91 @@ int rbe_cuda_search_multi(rbe_cuda_index* const* handles, uint32_t n_handles, co
                                partitions, accs, counts, stats);
     return guarded([&] {
         if (!handles || n_handles == 0 || !geometry) throw InvalidArgument("rbe_cuda_search_multi: null argument");
+        // lock every handle for the whole call, in address order (no lock-order inversion)
+        std::vector<rbe_cuda_index*> order(handles, handles + n_handles);
+        for (auto* h : order)
+            if (!h) throw InvalidArgument("rbe_cuda_search_multi: null handle");
+        std::sort(order.begin(), order.end());
+        if (std::adjacent_find(order.begin(), order.end()) != order.end())
+            throw InvalidArgument("rbe_cuda_search_multi: a handle appears twice");
+        std::vector<std::unique_lock<std::mutex>> locks;
+        for (auto* h : order) locks.emplace_back(h->mu);
+        // the reference rejects only an index whose total is empty (search.cpp:133-135);
+        // handles without documents take no part in the scan
+        uint64_t total = 0;
+        for (uint32_t h = 0; h < n_handles; ++h) total += handles[h]->total;
+        if (total == 0) throw InvalidArgument("search: empty index");
+        std::vector<rbe_cuda_index*> act;
         for (uint32_t h = 0; h < n_handles; ++h) {
-            std::lock_guard<std::mutex> lk(handles[h]->mu);
-            validate_search(handles[h], query_planes, geometry);
+            validate_shape(handles[h], query_planes, geometry);
+            if (handles[h]->total) act.push_back(handles[h]);
         }
         if (n_queries == 0) return;
         if (n == 0) {
             if (counts) std::fill(counts, counts + n_queries, 0);
+            if (stats) *stats = rbe_search_stats{};
             return;
         }
-        const int root = handles[0]->device;
+        if (!query_words || !scores || !ids || !partitions || !counts)
+            throw InvalidArgument("rbe_cuda_search_multi: null buffer");
         const size_t cells = size_t(n_queries) * n;
         const size_t list_bytes = sizeof(Result) * cells;
-        const size_t qbytes = size_t(n_queries) * query_planes * handles[0]->shape.wpp * 8;
-        rbe_search_stats total{};
-        std::vector<DevBuf> dq(n_handles), dres(n_handles);
-        DevBuf gathered, merged;
-        for (uint32_t h = 0; h < n_handles; ++h) {
-            DeviceGuard dg(handles[h]->device);
-            dq[h].ensure(qbytes);
-            dres[h].ensure(list_bytes);
-            RBE_CK(cudaMemcpy(dq[h].p, query_words, qbytes, cudaMemcpyHostToDevice));
-            rbe_search_stats st{};
-            const int rc = rbe_cuda_search_device(handles[h], dq[h].as<uint64_t>(), n_queries, query_planes, geometry,
-                                                  n, options, dres[h].as<rbe_result>(), nullptr, &st);
-            if (rc != RBE_CUDA_OK) {
-                if (rc == RBE_CUDA_EINVAL) throw InvalidArgument(g_last_error);
-                if (rc == RBE_CUDA_ERANGE) throw OutOfRange(g_last_error);
-                throw CudaError(g_last_error);
+        const size_t qbytes = size_t(n_queries) * query_planes * act[0]->shape.wpp * 8;
+        // 1. every device scans its partitions, concurrently: all batches are enqueued on
+        //    their handle's own stream before anything waits
+        std::vector<Pending> pend(act.size());
+        for (size_t h = 0; h < act.size(); ++h) {
+            rbe_cuda_index* ix = act[h];
+            DeviceGuard dg(ix->device);
+            cudaStream_t st = ix->stream;
+            ix->order.acquire(st);
+            ix->queries.ensure(qbytes);
+            RBE_CK(cudaMemcpyAsync(ix->queries.p, query_words, qbytes, cudaMemcpyHostToDevice, st));
+            pend[h] = enqueue_batch(ix, st, n_queries, query_planes, geometry, n, options);
+            ix->order.release(st);  // records the end of this handle's batch
+        }
+        // 2. the root gathers the lists peer-to-peer (after each handle's batch event) and merges
+        rbe_cuda_index* root = act[0];
+        const Result* merged_list = nullptr;
+        {
+            DeviceGuard dg(root->device);
+            cudaStream_t st = root->stream;
+            root->gathered.ensure(list_bytes * act.size());
+            root->merged.ensure(list_bytes);
+            for (size_t h = 0; h < act.size(); ++h) {
+                char* dst = static_cast<char*>(root->gathered.p) + h * list_bytes;
+                if (h) RBE_CK(cudaStreamWaitEvent(st, act[h]->order.done, 0));
+                RBE_CK(cudaMemcpyPeerAsync(dst, root->device, act[h]->out.p, act[h]->device, list_bytes, st));
             }
-            total.scored += st.scored;
-            total.candidates += st.candidates;
-            total.survivors += st.survivors;
-            total.variant = st.variant;
-            total.fallback |= st.fallback;
-            total.launches += st.launches;
-            total.scan_ms = std::max(total.scan_ms, st.scan_ms);
-            total.total_ms = std::max(total.total_ms, st.total_ms);
-        }
-        DeviceGuard dg(root);
-        gathered.ensure(list_bytes * n_handles);
-        merged.ensure(list_bytes);
-        for (uint32_t h = 0; h < n_handles; ++h)
-            RBE_CK(cudaMemcpyPeer(static_cast<char*>(gathered.p) + h * list_bytes, root, dres[h].p, handles[h]->device,
-                                  list_bytes));
-        const int rc = rbe_cuda_merge_device(root, gathered.as<rbe_result>(), n_handles, n_queries, n,
-                                             merged.as<rbe_result>(), nullptr);
-        if (rc != RBE_CUDA_OK) throw CudaError(g_last_error);
-        std::vector<Result> host(cells);
-        RBE_CK(cudaMemcpy(host.data(), merged.p, list_bytes, cudaMemcpyDeviceToHost));
-        for (uint32_t q = 0; q < n_queries; ++q) {
-            uint64_t c = 0;
-            for (uint64_t k = 0; k < n; ++k) {
-                const Result& r = host[size_t(q) * n + k];
-                if (!r.valid) break;
-                const size_t o = size_t(q) * n + k;
-                scores[o] = r.score;
-                ids[o] = r.id;
-                partitions[o] = r.partition;
-                if (accs) accs[o] = r.acc;
-                ++c;
+            if (act.size() > 1) {
+                enqueue_merge(root->gathered.as<Result>(), uint32_t(act.size()), n_queries, n, root->merged.as<Result>(),
+                              root->mtmp, root->mcnt, root->mscr, st);
+                merged_list = root->merged.as<Result>();
+            } else {
+                merged_list = root->gathered.as<Result>();
             }
-            counts[q] = c;
+            deliver(root, merged_list, n_queries, n, HostOut{scores, ids, partitions, accs, counts}, st);
+            root->order.release(st);  // root's scratch was used on its stream after its batch
         }
-        for (uint32_t h = 0; h < n_handles; ++h) {
-            DeviceGuard g2(handles[h]->device);
-            dq[h].release();
-            dres[h].release();
+        // 3. the other handles: their batches are complete (the root waited on them); read
+        //    their sticky flags (and stats)
+        rbe_search_stats tot{};
+        for (size_t h = 0; h < act.size(); ++h) {
+            rbe_cuda_index* ix = act[h];
+            DeviceGuard dg(ix->device);
+            rbe_search_stats s{};
+            finish_batch(ix, ix->stream, pend[h], &s);
+            tot.scored += s.scored;
+            tot.candidates += s.candidates;
+            tot.survivors += s.survivors;
+            tot.variant = s.variant;
+            tot.fallback |= s.fallback;
+            tot.launches += s.launches;
+            tot.scan_ms = std::max(tot.scan_ms, s.scan_ms);
+            tot.total_ms = std::max(tot.total_ms, s.total_ms);
         }
-        gathered.release();
-        merged.release();
-        if (stats) *stats = total;
+        if (act.size() > 1) tot.launches += 2;  // gather + merge select on the root
+        if (stats) *stats = tot;
     });
 }
 

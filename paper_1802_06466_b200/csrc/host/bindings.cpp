@@ -385,6 +385,94 @@ PYBIND11_MODULE(_core, m) {
         },
         py::arg("device"), py::arg("d_in"), py::arg("n_lists"), py::arg("n_queries"), py::arg("n"), py::arg("d_out"),
         py::arg("stream") = 0);
+    // --- local_select / global_select on the device (reference search.hpp:53-63)
+    m.def(
+        "local_select_arrays",
+        [](const DeviceIndex& d, py::array_t<uint64_t, py::array::c_style | py::array::forcecast> words,
+           uint32_t partition, const ScanGeometry& g) {
+            if (words.ndim() != 2) throw std::invalid_argument("local_select: words must be [planes][wpp]");
+            const auto [h, local] = d.locate(partition);
+            const uint64_t threads = uint64_t(g.blocks) * g.threads_per_block;
+            const uint64_t ql = std::min<uint64_t>(g.queue_length, g.items_per_thread);
+            py::array_t<double> scores({size_t(threads), size_t(ql)});
+            py::array_t<uint64_t> slots({size_t(threads), size_t(ql)});
+            py::array_t<uint32_t> counts(threads);
+            uint64_t scored = 0;
+            const rbe_scan_geometry geo{g.blocks, g.threads_per_block, g.items_per_thread, g.queue_length};
+            int status;
+            {
+                double* S = scores.mutable_data();
+                uint64_t* Z = slots.mutable_data();
+                uint32_t* C = counts.mutable_data();
+                py::gil_scoped_release nogil;
+                status = rbe_cuda_local_select(d.handle(h), local, words.data(), uint32_t(words.shape(0)), &geo, S, Z,
+                                               C, &scored);
+            }
+            ck(status);
+            return py::make_tuple(scores, slots, counts, scored);
+        },
+        py::arg("index"), py::arg("words"), py::arg("partition"), py::arg("geometry"),
+        "local_select on the device -> (scores[threads][ql], slots[threads][ql], counts[threads], scored)");
+    m.def(
+        "local_select",
+        [](const RbeEmbedding& query, py::object index, uint32_t partition, const ScanGeometry& g) {
+            std::vector<std::vector<Candidate>> lists;
+            if (py::isinstance<DeviceIndex>(index)) {
+                const DeviceIndex& d = index.cast<const DeviceIndex&>();
+                py::gil_scoped_release nogil;
+                lists = local_select(query, d, partition, g);
+            } else {
+                const KeywordIndex& k = index.cast<const KeywordIndex&>();
+                py::gil_scoped_release nogil;
+                lists = local_select(query, k, partition, g);
+            }
+            py::list out;
+            for (const auto& l : lists) {
+                py::list row;
+                for (const Candidate& c : l) row.append(py::make_tuple(c.score, c.slot));
+                out.append(row);
+            }
+            return out;
+        },
+        py::arg("query"), py::arg("index"), py::arg("partition"), py::arg("geometry"),
+        "Per-logical-thread [(score, slot)] lists of one partition (reference local_select)");
+    m.def(
+        "select_topn",
+        [](py::array_t<double, py::array::c_style | py::array::forcecast> scores,
+           py::array_t<uint64_t, py::array::c_style | py::array::forcecast> ids, uint32_t partition, uint64_t n,
+           int device) {
+            if (scores.size() != ids.size()) throw std::invalid_argument("select_topn: scores and ids differ in size");
+            const uint64_t m = std::min<uint64_t>(n, uint64_t(scores.size()));
+            py::array_t<double> os(m);
+            py::array_t<uint64_t> oi(m);
+            uint64_t got = 0;
+            int status;
+            {
+                double* S = os.mutable_data();
+                uint64_t* I = oi.mutable_data();
+                py::gil_scoped_release nogil;
+                status = rbe_cuda_select_topn(device, scores.data(), ids.data(), uint64_t(scores.size()), partition, n,
+                                              S, I, &got);
+            }
+            ck(status);
+            return py::make_tuple(os[py::slice(0, got, 1)], oi[py::slice(0, got, 1)]);
+        },
+        py::arg("scores"), py::arg("ids"), py::arg("partition"), py::arg("n"), py::arg("device") = 0,
+        "global_select's selection on the device: top n (score desc, id asc) -> (scores, ids)");
+    m.def(
+        "index_check",
+        [](uintptr_t handle) {
+            int status;
+            {
+                py::gil_scoped_release nogil;
+                status = rbe_cuda_index_check(reinterpret_cast<rbe_cuda_index*>(handle));
+            }
+            ck(status);
+        },
+        py::arg("handle"));
+    m.def(
+        "index_inject_error", [](uintptr_t handle) { ck(rbe_cuda_index_inject_error(reinterpret_cast<rbe_cuda_index*>(handle))); },
+        py::arg("handle"), "test hook: set the index's sticky internal-consistency flag");
     m.attr("RESULT_RECORD_BYTES") = sizeof(rbe_result);
     m.def("version", [] { return std::string(rbe_cuda_version()); });
 }

@@ -9,8 +9,10 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "rbe/binary_vector.hpp"
 #include "rbe/embedding.hpp"
@@ -413,10 +415,22 @@ Partition DeviceIndex::download_partition(uint32_t partition) const {
     return p;
 }
 
+std::pair<size_t, uint32_t> DeviceIndex::locate(uint32_t partition) const {
+    if (partition >= partitions_) throw std::out_of_range("partition out of range");
+    const int h = part_handle_[partition];
+    if (h < 0) throw std::out_of_range("partition not resident in this process");
+    return {size_t(h), part_local_[partition]};
+}
+
+uint64_t DeviceIndex::partition_size(uint32_t partition) const {
+    if (partition >= partitions_) throw std::out_of_range("partition out of range");
+    return part_count_[partition];
+}
+
 std::vector<SelectionResult> DeviceIndex::search_words(std::span<const uint64_t> query_words, uint32_t n_queries,
                                                        uint32_t query_planes, const ScanGeometry& g, uint64_t n,
-                                                       SearchStats* stats, ScanVariant variant,
-                                                       uint32_t probe_tiles) const {
+                                                       SearchStats* stats, ScanVariant variant, uint32_t probe_tiles,
+                                                       std::vector<std::vector<int64_t>>* acc_out) const {
     const size_t wpp = PackedBinaryVector::words_for(dim_);
     if (query_words.size() != size_t(n_queries) * query_planes * wpp)
         throw std::invalid_argument("search: query buffer size does not match (Q, planes, dim)");
@@ -438,13 +452,15 @@ std::vector<SelectionResult> DeviceIndex::search_words(std::span<const uint64_t>
     // device (rbe_cuda_search_multi).
     ck(rbe_cuda_search_multi(hs.data(), uint32_t(hs.size()), query_words.data(), n_queries, query_planes, &geo, n,
                              &opt, scores.data(), ids.data(), parts.data(), accs.data(), counts.data(), &st));
+    if (acc_out) acc_out->assign(n_queries, {});
     for (uint32_t q = 0; q < n_queries; ++q) {
         auto& e = out[q].entries;
         e.resize(counts[q]);
         for (uint64_t k = 0; k < counts[q]; ++k) {
             const size_t o = size_t(q) * n + k;
-            e[k] = SelectionEntry{scores[o], ids[o], parts[o], accs[o]};
+            e[k] = SelectionEntry{scores[o], ids[o], parts[o]};
         }
+        if (acc_out) (*acc_out)[q].assign(accs.begin() + size_t(q) * n, accs.begin() + size_t(q) * n + counts[q]);
     }
     if (stats) {
         stats->scored += st.scored;
@@ -504,6 +520,72 @@ std::vector<uint64_t> flatten(std::span<const RbeEmbedding> qs, uint32_t dim, ui
 
 }  // namespace
 
+std::vector<std::vector<Candidate>> local_select(const RbeEmbedding& query, const DeviceIndex& index,
+                                                 uint32_t partition, const ScanGeometry& geometry,
+                                                 SearchStats* stats) {
+    check_query(query, index.dim());
+    const auto [h, local] = index.locate(partition);
+    if (geometry.queue_length == 0) throw std::invalid_argument("local_select: queue_length must be positive");
+    const uint64_t threads = uint64_t(geometry.blocks) * geometry.threads_per_block;
+    const uint64_t ql = std::min<uint64_t>(geometry.queue_length, geometry.items_per_thread);
+    std::vector<uint64_t> words;
+    for (const auto& p : query.planes) words.insert(words.end(), p.words.begin(), p.words.end());
+    std::vector<double> scores(threads * ql);
+    std::vector<uint64_t> slots(threads * ql);
+    std::vector<uint32_t> counts(threads);
+    uint64_t scored = 0;
+    const rbe_scan_geometry geo{geometry.blocks, geometry.threads_per_block, geometry.items_per_thread,
+                                geometry.queue_length};
+    ck(rbe_cuda_local_select(index.handle(h), local, words.data(), uint32_t(query.planes.size()), &geo,
+                             scores.data(), slots.data(), counts.data(), &scored));
+    std::vector<std::vector<Candidate>> lists(threads);
+    for (uint64_t t = 0; t < threads; ++t) {
+        lists[t].reserve(geometry.queue_length);
+        for (uint32_t k = 0; k < counts[t]; ++k) lists[t].push_back(Candidate{scores[t * ql + k], slots[t * ql + k]});
+    }
+    if (stats) stats->scored += scored;
+    return lists;
+}
+
+std::vector<std::vector<Candidate>> local_select(const RbeEmbedding& query, const KeywordIndex& index,
+                                                 uint32_t partition, const ScanGeometry& geometry,
+                                                 SearchStats* stats) {
+    check_query(query, index.dim);
+    if (geometry.queue_length == 0) throw std::invalid_argument("local_select: queue_length must be positive");
+    const Partition& part = index.partitions.at(partition);
+    if (geometry.capacity() < part.count) throw std::invalid_argument("local_select: geometry does not cover partition");
+    // a one-partition device copy of just this partition (ordinal kept)
+    KeywordIndex one;
+    one.dim = index.dim;
+    one.keyword_planes = index.keyword_planes;
+    one.residual_weights = index.residual_weights;
+    one.partitions.push_back(part);
+    DeviceIndex dev(one, {0});
+    return local_select(query, dev, 0, geometry, stats);
+}
+
+SelectionResult global_select(const std::vector<std::vector<Candidate>>& per_thread, const Partition& partition,
+                              uint32_t partition_ordinal, uint64_t n) {
+    std::vector<double> scores;
+    std::vector<uint64_t> ids;
+    for (const auto& list : per_thread)
+        for (const Candidate& c : list) {
+            scores.push_back(c.score);
+            ids.push_back(partition.ids.at(c.slot));  // slot -> id (search.cpp:121-122)
+        }
+    SelectionResult r;
+    if (scores.empty() || n == 0) return r;
+    const uint64_t m = std::min<uint64_t>(n, scores.size());
+    std::vector<double> os(m);
+    std::vector<uint64_t> oi(m);
+    uint64_t got = 0;
+    ck(rbe_cuda_select_topn(0, scores.data(), ids.data(), scores.size(), partition_ordinal, n, os.data(), oi.data(),
+                            &got));
+    r.entries.resize(got);
+    for (uint64_t k = 0; k < got; ++k) r.entries[k] = SelectionEntry{os[k], oi[k], partition_ordinal};
+    return r;
+}
+
 std::vector<SelectionResult> search_batch(std::span<const RbeEmbedding> queries, const DeviceIndex& index,
                                           const ScanGeometry& geometry, uint64_t n, SearchStats* stats) {
     if (index.total_keywords() == 0) throw std::invalid_argument("search: empty index");
@@ -518,12 +600,59 @@ SelectionResult search(const RbeEmbedding& query, const DeviceIndex& index, cons
     return search_batch(std::span<const RbeEmbedding>(&query, 1), index, geometry, n, stats).at(0);
 }
 
+namespace {
+
+// The drop-in search(query, KeywordIndex, ...) keeps the device copy of the last
+// index it saw, so a reference-style loop of per-query calls uploads once.  The
+// KeywordIndex is immutable after build; the key is its shape plus
+// the address, size and first/last words of every array, so a rebuilt or resized
+// index is re-uploaded.
+std::vector<uint64_t> fingerprint(const KeywordIndex& k) {
+    std::vector<uint64_t> f{k.dim, k.keyword_planes, k.residual_weights ? 1u : 0u, k.partitions.size()};
+    auto add = [&](const void* p, size_t n, uint64_t first, uint64_t last) {
+        f.push_back(reinterpret_cast<uintptr_t>(p));
+        f.push_back(n);
+        f.push_back(first);
+        f.push_back(last);
+    };
+    for (const Partition& p : k.partitions) {
+        f.push_back(p.count);
+        for (const auto& b : p.plane_blocks) add(b.data(), b.size(), b.empty() ? 0 : b.front(), b.empty() ? 0 : b.back());
+        add(p.magnitudes.data(), p.magnitudes.size(), 0, 0);
+        add(p.ids.data(), p.ids.size(), p.ids.empty() ? 0 : p.ids.front(), p.ids.empty() ? 0 : p.ids.back());
+    }
+    return f;
+}
+
+struct DropInCache {
+    std::mutex mu;
+    std::vector<uint64_t> key;
+    std::shared_ptr<DeviceIndex> dev;
+};
+DropInCache& drop_in_cache() {
+    static DropInCache* c = new DropInCache();  // process lifetime (no teardown-order races)
+    return *c;
+}
+
+}  // namespace
+
 SelectionResult search(const RbeEmbedding& query, const KeywordIndex& index, const ScanGeometry& geometry, uint64_t n,
                        SearchStats* stats) {
     if (index.partitions.empty() || index.total_keywords() == 0) throw std::invalid_argument("search: empty index");
     check_query(query, index.dim);
-    DeviceIndex dev(index, {0});
-    return search(query, dev, geometry, n, stats);
+    std::shared_ptr<DeviceIndex> dev;
+    {
+        DropInCache& c = drop_in_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        std::vector<uint64_t> key = fingerprint(index);
+        if (!c.dev || c.key != key) {
+            c.dev.reset();
+            c.dev = std::make_shared<DeviceIndex>(index, std::vector<int>{0});
+            c.key = std::move(key);
+        }
+        dev = c.dev;
+    }
+    return search(query, *dev, geometry, n, stats);
 }
 
 }  // namespace rbe

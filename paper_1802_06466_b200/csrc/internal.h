@@ -73,6 +73,12 @@ struct ScanArgs {
     unsigned int* overflow = nullptr;          // [1]
     unsigned int* error = nullptr;             // [1] internal consistency failures (tensor scan)
     float mag_lo = 0.0f, mag_hi = 0.0f;        // magnitude range of the index (tensor threshold bins)
+    // local_select output (exact kernel, one query, one partition): per logical thread
+    // t = block * T_b + thread its list [t * ql_eff, + list_counts[t]) of (score, slot),
+    // ordered by (score desc, slot asc) like BoundedQueue (search.cpp:32-48)
+    double* list_scores = nullptr;
+    uint64_t* list_slots = nullptr;
+    uint32_t* list_counts = nullptr;
 };
 
 // ---- exact kernel (scan_exact.cu)

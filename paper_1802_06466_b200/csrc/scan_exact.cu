@@ -139,10 +139,18 @@ __global__ void __launch_bounds__(kThreads) scan_exact_kernel(ScanArgs a, uint32
             }
             ++scored;
         }
+        if (a.list_counts) {  // local_select: the per-thread lists themselves (query 0)
+            a.list_counts[gt] = size[0];
+            for (uint32_t k = 0; k < size[0]; ++k) {
+                const QueueEntry& e = ql_eff == 1 ? best[0] : qs[0][k];
+                a.list_scores[gt * ql_eff + k] = e.score;
+                a.list_slots[gt * ql_eff + k] = e.slot;
+            }
+        }
 #pragma unroll
         for (int j = 0; j < QG; ++j) {
             const uint32_t qi = q0 + j;
-            if (qi >= a.Q) continue;
+            if (qi >= a.Q || a.list_counts) continue;
             for (uint32_t k = 0; k < size[j]; ++k) {
                 const QueueEntry& e = ql_eff == 1 ? best[j] : qs[j][k];
                 const unsigned long long pos = atomicAdd(a.surv_count + qi, 1ull);

@@ -96,8 +96,6 @@ struct TensorParams {
     uint32_t w32;                  // u32 words per doc plane (= data K blocks)
     uint32_t nstages;              // ring depth (stages of sw docs)
     uint32_t nwg;                  // worker warpgroups (2 or 3)
-    uint32_t dbg;                  // debugging/timing experiments (RBE_DBG): 1 = epilogue skips TMEM loads,
-                                   // 2 = expand skips TMEM stores (results invalid)
     int32_t f16max;                // F <= f16max - c_q for every pair: the low 16 bits keep the sign of any
                                    // F >= 0 when c_q <= 32767 - f16max (pack::16b epilogue); 0 = never
     uint32_t sw;                   // strip width in logical threads (128 or 256) = docs per stage
@@ -1466,7 +1464,6 @@ TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geom
     pl.qp = qp;
     pl.n = n;
     pl.probe_tiles = probe_tiles ? probe_tiles : 8;
-    if (const char* e = getenv("RBE_PROBE_TILES")) pl.probe_tiles = uint32_t(atoi(e));  // tuning experiments
     pl.prefix.assign(counts.size() + 1, 0);
     const uint64_t threads = uint64_t(g.blocks) * g.threads_per_block;
     for (size_t i = 0; i < counts.size(); ++i) {
@@ -1529,7 +1526,6 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.w32 = s.w32;
     tp.sw = strip_width(g_of(a));
     tp.nwg = pick_nwg(s.w32);
-    if (const char* e = getenv("RBE_DBG")) tp.dbg = uint32_t(atoi(e));
     {
         // D_sigma <= sigma * vmax * K * rqmax; the packed epilogue is used per strip when every live
         // query's c_q keeps that bound + c_q within int16
@@ -1563,9 +1559,15 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.n = plan.n;
     if (n_strips == 0) return launches;
     const int grid = int(std::min<uint64_t>(n_strips, uint64_t(sm_count())));
+#ifdef RBE_PHASE_PROF
+    // profiling builds only (RBE_NVCC_EXTRA=-DRBE_PHASE_PROF): per-warp phase cycles, printed per batch
     static unsigned long long* d_prof = nullptr;
-    const bool prof = getenv("RBE_PROF") != nullptr;
-    if (prof && !d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 2048 * 16 * 8));
+    const bool prof = true;
+    if (!d_prof) RBE_CK(cudaMalloc(&d_prof, sizeof(unsigned long long) * 2048 * 16 * 8));
+#else
+    constexpr bool prof = false;
+    unsigned long long* d_prof = nullptr;
+#endif
     for (uint32_t ps = 0; ps < passes; ++ps) {
         tp.q0 = ps * kQPass;
         tp.nq = std::min<uint32_t>(kQPass, Q - tp.q0);

@@ -60,3 +60,18 @@ def test_no_gpu_fails_loudly():
     assert b"no CPU fallback" in lib.rbe_cuda_last_error()
     rc = lib.rbe_cuda_index_create(C.byref(Shape(0, 2, 1)), 1, ords, counts, 0, C.byref(h))
     assert rc == 1  # EINVAL checked before touching the device
+
+
+def test_ctypes_binding_declares_only_exported_symbols():
+    """The reference-side ctypes binding (tests/rbe_ctypes.py, shown in INTEGRATION.md)
+    loads on CPU and every function it types is exported and declared in the header."""
+    from tests import rbe_ctypes
+
+    lib = rbe_ctypes.load()
+    typed = [n for n in dir(lib) if n.startswith("rbe_cuda_")]
+    names = set(declared())
+    for n in ("rbe_cuda_index_create", "rbe_cuda_index_upload_partition", "rbe_cuda_search",
+              "rbe_cuda_index_destroy", "rbe_cuda_last_error"):
+        assert n in names
+        assert getattr(lib, n).argtypes is not None
+    assert all(n in names for n in typed)
