@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <memory>
 #include <span>
+#include <string>
 #include <vector>
 
 #include "rbe/index.hpp"
@@ -55,6 +56,12 @@ struct SearchStats {
 
 enum class ScanVariant : uint32_t { Auto = 0, Exact = 1, Tensor = 2 };
 
+/// Ingest statistics of DeviceIndex::from_rbei.
+struct LoadStats {
+    uint64_t file_bytes = 0;  // partition bytes read from the file
+    double seconds = 0.0;     // wall time (all devices)
+};
+
 /// The HBM-resident index: partition p lives on devices[p % devices.size()].
 class DeviceIndex {
 public:
@@ -64,6 +71,13 @@ public:
     static DeviceIndex synthetic(uint32_t dim, uint32_t keyword_planes, bool residual_weights, uint64_t n_docs,
                                  uint32_t partitions, uint64_t seed, std::vector<int> devices = {0},
                                  uint32_t rank = 0, uint32_t world = 1);
+    /// RBEI v1 file straight into HBM: the reference's load_index
+    /// (src/index.cpp:170-208) plus the upload in one streamed pass -- pread by host
+    /// threads into page-locked staging, copy, re-pack on the device.  Partition p goes to
+    /// devices[p % devices.size()]; the devices are loaded concurrently.  Same errors as
+    /// load_index (std::runtime_error); magnitudes must be finite and > 0.
+    static DeviceIndex from_rbei(const std::string& path, std::vector<int> devices = {0}, uint32_t io_threads = 0,
+                                 LoadStats* stats = nullptr);
     ~DeviceIndex();
     DeviceIndex(DeviceIndex&&) noexcept;
     DeviceIndex& operator=(DeviceIndex&&) noexcept;

@@ -116,6 +116,33 @@ int rbe_cuda_index_create(const rbe_index_shape* shape, uint32_t n_partitions, c
  * reference's load_index does not validate). */
 int rbe_cuda_index_upload_partition(rbe_cuda_index* index, uint32_t i, const uint64_t* planes,
                                     const float* mags, const uint64_t* ids);
+/* (Streamed in chunks through page-locked staging buffers filled by several host
+ * threads; each chunk is re-packed into the store layout on the device.) */
+
+/* RBEI v1 ingest.  Replaces the reference's load_index
+ * (src/index.cpp:170-208) followed by an upload: the file is read once, straight
+ * into HBM.  Same errors as load_index (ERUNTIME): "cannot open index: <path>",
+ * "not an RBEI index file: <path>", "unsupported index version", "truncated index
+ * file: <path>". */
+typedef struct {
+    uint64_t file_bytes_read; /* partition bytes read from the file            */
+    double seconds;           /* wall time of the call                         */
+} rbe_load_stats;
+
+/* Header only: shape, partition count and (up to counts_cap) partition sizes.
+ * Host-only (no GPU needed). */
+int rbe_cuda_rbei_header(const char* path, rbe_index_shape* shape, uint32_t* n_partitions,
+                         uint64_t* counts, uint32_t counts_cap);
+
+/* A handle on `device` holding the file's partitions `partitions[0..n)` (n = 0:
+ * all of them, in order) as its local partitions 0..n-1 with their file ordinals.
+ * The partition blocks are read with pread by `io_threads` host threads (0 =
+ * min(16, hardware threads)) into two alternating page-locked staging buffers
+ * (64 MB chunks of documents), copied to the device and re-packed there.
+ * Magnitudes must be finite and > 0 (EINVAL). `stats` may be NULL. */
+int rbe_cuda_index_open_rbei(const char* path, const uint32_t* partitions, uint32_t n_partitions,
+                             int device, uint32_t io_threads, rbe_cuda_index** out,
+                             rbe_load_stats* stats);
 
 /* Fill every local partition on the device with the synthetic corpus of
  * global doc g of n_total, bits from counter-based

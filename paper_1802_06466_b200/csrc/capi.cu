@@ -13,8 +13,14 @@
 //    per batch, and the next synchronous call on the index (rbe_cuda_search,
 //    search_device with stats, last_batch_ms, search_multi) reports it.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <thread>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -500,6 +506,197 @@ void rethrow_status(int rc) {
 
 }  // namespace
 
+namespace {
+
+// ---------------------------------------------------------------- ingest
+// One partition in the reference's natural layout (Partition::plane_blocks [kp][count][wpp]
+// u64, magnitudes f32, ids u64; index.hpp:16-21) streamed into HBM in chunks of documents:
+// the host fills a page-locked staging buffer per chunk (from memory or from an RBEI file, with
+// several host threads), the chunk's plane words are copied to a device staging buffer and
+// re-packed into the store layout by the device, magnitudes and ids are copied in place.  Two
+// staging buffers alternate, so the host fill of chunk c + 1 overlaps the copies and the repack
+// of chunk c.
+struct ChunkSource {
+    virtual ~ChunkSource() = default;
+    // write docs [z0, z0 + n): plane words [kp][n][wpp], then n f32 magnitudes, then n u64 ids
+    virtual void fill(uint8_t* dst, uint64_t z0, uint64_t n) = 0;
+};
+
+// run `pieces` (byte-range copies) on up to `threads` host threads
+struct Piece {
+    uint8_t* dst;
+    uint64_t off;  // file offset, or source address for memory copies
+    size_t len;
+};
+template <typename F>
+void run_pieces(std::vector<Piece>& pieces, uint32_t threads, F&& copy) {
+    std::vector<Piece> split;
+    constexpr size_t kPiece = size_t(8) << 20;
+    for (const Piece& pc : pieces)
+        for (size_t o = 0; o < pc.len; o += kPiece)
+            split.push_back(Piece{pc.dst + o, pc.off + o, std::min(kPiece, pc.len - o)});
+    const uint32_t T = std::max<uint32_t>(1, std::min<uint32_t>(threads, uint32_t(split.size())));
+    if (T == 1) {
+        for (const Piece& pc : split) copy(pc);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::vector<std::exception_ptr> errs(T);
+    for (uint32_t t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            try {
+                for (size_t k = t; k < split.size(); k += T) copy(split[k]);
+            } catch (...) {
+                errs[t] = std::current_exception();
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+}
+
+std::vector<Piece> chunk_pieces(uint8_t* dst, uint64_t planes0, uint64_t mags0, uint64_t ids0, uint64_t count,
+                                uint32_t kp, uint32_t wpp, uint64_t z0, uint64_t n) {
+    std::vector<Piece> v;
+    for (uint32_t t = 0; t < kp; ++t)
+        v.push_back(Piece{dst + size_t(t) * n * wpp * 8, planes0 + (uint64_t(t) * count + z0) * wpp * 8, size_t(n) * wpp * 8});
+    uint8_t* m = dst + size_t(kp) * n * wpp * 8;
+    v.push_back(Piece{m, mags0 + z0 * 4, size_t(n) * 4});
+    v.push_back(Piece{m + n * 4, ids0 + z0 * 8, size_t(n) * 8});
+    return v;
+}
+
+struct MemorySource : ChunkSource {
+    const uint64_t* planes;
+    const float* mags;
+    const uint64_t* ids;
+    uint64_t count;
+    uint32_t kp, wpp, threads;
+    void fill(uint8_t* dst, uint64_t z0, uint64_t n) override {
+        auto pcs = chunk_pieces(dst, uint64_t(uintptr_t(planes)), uint64_t(uintptr_t(mags)), uint64_t(uintptr_t(ids)),
+                                count, kp, wpp, z0, n);
+        run_pieces(pcs, threads, [](const Piece& pc) {
+            std::memcpy(pc.dst, reinterpret_cast<const void*>(uintptr_t(pc.off)), pc.len);
+        });
+    }
+};
+
+struct FileSource : ChunkSource {
+    int fd = -1;
+    std::string path;
+    uint64_t planes0, mags0, ids0, count;
+    uint32_t kp, wpp, threads;
+    uint64_t* bytes_read = nullptr;
+    void fill(uint8_t* dst, uint64_t z0, uint64_t n) override {
+        auto pcs = chunk_pieces(dst, planes0, mags0, ids0, count, kp, wpp, z0, n);
+        run_pieces(pcs, threads, [&](const Piece& pc) {
+            size_t done = 0;
+            while (done < pc.len) {
+                const ssize_t r = ::pread(fd, pc.dst + done, pc.len - done, off_t(pc.off + done));
+                if (r < 0 && errno == EINTR) continue;
+                if (r <= 0) throw std::runtime_error("truncated index file: " + path);
+                done += size_t(r);
+            }
+        });
+        for (const Piece& pc : pcs) *bytes_read += pc.len;
+    }
+};
+
+void stream_partition(rbe_cuda_index* ix, uint32_t i, ChunkSource& src) {
+    auto& L = ix->parts[i];
+    if (L.count == 0) return;
+    const Shape& s = ix->shape;
+    cudaStream_t st = ix->stream;
+    const size_t plane_doc = size_t(s.kp) * s.wpp * 8, per_doc = plane_doc + 12;
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(L.count, (size_t(64) << 20) / per_doc));
+    struct Host {
+        uint8_t* p = nullptr;
+        ~Host() {
+            if (p) cudaFreeHost(p);
+        }
+    } host[2];
+    DevBuf dnat[2];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    struct Events {
+        cudaEvent_t* e;
+        ~Events() {
+            for (int k = 0; k < 2; ++k)
+                if (e[k]) cudaEventDestroy(e[k]);
+        }
+    } ev_guard{ev};
+    for (int k = 0; k < 2; ++k) {
+        RBE_CK(cudaMallocHost(&host[k].p, chunk * per_doc));
+        dnat[k].ensure(chunk * plane_doc);
+        RBE_CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    }
+    ix->order.acquire(st);
+    uint64_t c = 0;
+    for (uint64_t z0 = 0; z0 < L.count; z0 += chunk, ++c) {
+        const int k = int(c & 1);
+        const uint64_t n = std::min(chunk, L.count - z0);
+        if (c >= 2) RBE_CK(cudaEventSynchronize(ev[k]));  // staging k free again
+        src.fill(host[k].p, z0, n);
+        RBE_CK(cudaMemcpyAsync(dnat[k].p, host[k].p, n * plane_doc, cudaMemcpyHostToDevice, st));
+        RBE_CK(cudaMemcpyAsync(L.mags + z0, host[k].p + n * plane_doc, n * 4, cudaMemcpyHostToDevice, st));
+        RBE_CK(cudaMemcpyAsync(L.ids + z0, host[k].p + n * plane_doc + n * 4, n * 8, cudaMemcpyHostToDevice, st));
+        // chunk [z0, z0 + n) of the store: plane t of doc z lives at (t count_pad + z) w32
+        launch_repack_planes(dnat[k].as<uint64_t>(), L.planes + z0 * s.w32, n, L.count_pad, s, ix->perm, st);
+        RBE_CK(cudaEventRecord(ev[k], st));
+    }
+    ix->mag_range_ok = false;
+    ix->counters.ensure(64);
+    RBE_CK(cudaMemsetAsync(ix->counters.p, 0, 4, st));
+    launch_validate_mags(L.mags, L.count, ix->counters.as<uint32_t>(), st);
+    uint32_t* bad = reinterpret_cast<uint32_t*>(ix->host_out);
+    RBE_CK(cudaMemcpyAsync(bad, ix->counters.p, 4, cudaMemcpyDeviceToHost, st));
+    ix->order.release(st);
+    RBE_CK(cudaStreamSynchronize(st));
+    if (*bad) throw InvalidArgument("keyword magnitudes must be finite and > 0");
+}
+
+uint32_t default_io_threads() { return std::max(1u, std::min(16u, std::thread::hardware_concurrency())); }
+
+// RBEI v1 header ("RBEI", u32 version, dim, kp, rw, P, u64 count[P]), read the
+// way the reference's load_index reads it (src/index.cpp:170-189), with the same errors
+struct RbeiHeader {
+    rbe_index_shape shape{};
+    std::vector<uint64_t> counts;
+    uint64_t data_offset = 0;  // first byte of partition 0
+    uint64_t file_bytes = 0;
+};
+
+RbeiHeader read_rbei_header(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open index: " + path);
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "RBEI", 4) != 0)
+        throw std::runtime_error("not an RBEI index file: " + path);
+    uint32_t h[5];
+    if (std::fread(h, 4, 5, f) != 5) throw std::runtime_error("truncated index file: " + path);
+    if (h[0] != 1) throw std::runtime_error("unsupported index version");
+    RbeiHeader r;
+    r.shape.dim = h[1];
+    r.shape.keyword_planes = h[2];
+    r.shape.residual_weights = h[3] != 0;
+    r.counts.resize(h[4]);
+    if (h[4] && std::fread(r.counts.data(), 8, h[4], f) != h[4]) throw std::runtime_error("truncated index file: " + path);
+    r.data_offset = 4 + 5 * 4 + uint64_t(h[4]) * 8;
+    struct stat sb;
+    if (::stat(path.c_str(), &sb) != 0) throw std::runtime_error("cannot open index: " + path);
+    r.file_bytes = uint64_t(sb.st_size);
+    const uint64_t wpp = (uint64_t(r.shape.dim) + 63) / 64;
+    uint64_t end = r.data_offset;
+    for (uint64_t c : r.counts) end += c * (uint64_t(r.shape.keyword_planes) * wpp * 8 + 12);
+    if (end > r.file_bytes) throw std::runtime_error("truncated index file: " + path);
+    return r;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* rbe_cuda_last_error(void) { return g_last_error.c_str(); }
@@ -569,6 +766,7 @@ int rbe_cuda_index_create(const rbe_index_shape* shape, uint32_t n_partitions, c
     });
 }
 
+
 int rbe_cuda_index_upload_partition(rbe_cuda_index* ix, uint32_t i, const uint64_t* planes, const float* mags,
                                     const uint64_t* ids) {
     return guarded([&] {
@@ -579,25 +777,95 @@ int rbe_cuda_index_upload_partition(rbe_cuda_index* ix, uint32_t i, const uint64
         auto& L = ix->parts[i];
         if (L.count == 0) return;
         if (!planes || !mags || !ids) throw InvalidArgument("rbe_cuda_index_upload_partition: null buffer");
-        const Shape& s = ix->shape;
-        cudaStream_t st = ix->stream;
-        ix->order.acquire(st);
-        const size_t nat_bytes = size_t(s.kp) * L.count * s.wpp * 8;
-        DevBuf tmp;
-        tmp.ensure(nat_bytes + 64);
-        RBE_CK(cudaMemcpyAsync(tmp.p, planes, nat_bytes, cudaMemcpyHostToDevice, st));
-        launch_repack_planes(tmp.as<uint64_t>(), L.planes, L.count, L.count_pad, s, ix->perm, st);
-        ix->mag_range_ok = false;
-        RBE_CK(cudaMemcpyAsync(L.mags, mags, L.count * 4, cudaMemcpyHostToDevice, st));
-        RBE_CK(cudaMemcpyAsync(L.ids, ids, L.count * 8, cudaMemcpyHostToDevice, st));
-        ix->counters.ensure(64);
-        RBE_CK(cudaMemsetAsync(ix->counters.p, 0, 4, st));
-        launch_validate_mags(L.mags, L.count, ix->counters.as<uint32_t>(), st);
-        uint32_t* bad = reinterpret_cast<uint32_t*>(ix->host_out);
-        RBE_CK(cudaMemcpyAsync(bad, ix->counters.p, 4, cudaMemcpyDeviceToHost, st));
-        ix->order.release(st);
-        RBE_CK(cudaStreamSynchronize(st));
-        if (*bad) throw InvalidArgument("rbe_cuda_index_upload_partition: keyword magnitudes must be finite and > 0");
+        MemorySource src;
+        src.planes = planes;
+        src.mags = mags;
+        src.ids = ids;
+        src.count = L.count;
+        src.kp = ix->shape.kp;
+        src.wpp = ix->shape.wpp;
+        src.threads = default_io_threads();
+        try {
+            stream_partition(ix, i, src);
+        } catch (const InvalidArgument& e) {
+            throw InvalidArgument(std::string("rbe_cuda_index_upload_partition: ") + e.what());
+        }
+    });
+}
+
+int rbe_cuda_rbei_header(const char* path, rbe_index_shape* shape, uint32_t* n_partitions, uint64_t* counts,
+                         uint32_t counts_cap) {
+    return guarded([&] {
+        if (!path || !shape || !n_partitions) throw InvalidArgument("rbe_cuda_rbei_header: null argument");
+        const RbeiHeader h = read_rbei_header(path);
+        *shape = h.shape;
+        *n_partitions = uint32_t(h.counts.size());
+        if (counts)
+            for (uint32_t p = 0; p < std::min<uint32_t>(counts_cap, uint32_t(h.counts.size())); ++p) counts[p] = h.counts[p];
+    });
+}
+
+int rbe_cuda_index_open_rbei(const char* path, const uint32_t* partitions, uint32_t n_partitions, int device,
+                             uint32_t io_threads, rbe_cuda_index** out, rbe_load_stats* stats) {
+    return guarded([&] {
+        if (!path || !out || (n_partitions && !partitions)) throw InvalidArgument("rbe_cuda_index_open_rbei: null argument");
+        const auto t0 = std::chrono::steady_clock::now();
+        const RbeiHeader h = read_rbei_header(path);
+        std::vector<uint32_t> sel;
+        if (n_partitions) sel.assign(partitions, partitions + n_partitions);
+        else
+            for (uint32_t p = 0; p < h.counts.size(); ++p) sel.push_back(p);
+        std::vector<uint64_t> counts;
+        for (uint32_t p : sel) {
+            if (p >= h.counts.size()) throw OutOfRange("rbe_cuda_index_open_rbei: partition out of range");
+            counts.push_back(h.counts[p]);
+        }
+        rbe_cuda_index* raw = nullptr;
+        const int rc = rbe_cuda_index_create(&h.shape, uint32_t(sel.size()), sel.data(), counts.data(), device, &raw);
+        if (rc != RBE_CUDA_OK) {
+            const std::string msg = g_last_error;
+            if (rc == RBE_CUDA_EINVAL) throw InvalidArgument(msg);
+            if (rc == RBE_CUDA_ERANGE) throw OutOfRange(msg);
+            throw std::runtime_error(msg);
+        }
+        std::unique_ptr<rbe_cuda_index> ix(raw);
+        const int fd = ::open(path, O_RDONLY);
+        if (fd < 0) throw std::runtime_error("cannot open index: " + std::string(path));
+        struct Fd {
+            int fd;
+            ~Fd() { ::close(fd); }
+        } fd_guard{fd};
+        ::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
+        // partition byte offsets in the file (partitions are stored back to back)
+        const uint64_t wpp = ix->shape.wpp, kp = ix->shape.kp;
+        std::vector<uint64_t> poff(h.counts.size() + 1, h.data_offset);
+        for (size_t p = 0; p < h.counts.size(); ++p) poff[p + 1] = poff[p] + h.counts[p] * (kp * wpp * 8 + 12);
+        uint64_t bytes = 0;
+        DeviceGuard dg(device);
+        std::lock_guard<std::mutex> lk(ix->mu);
+        for (size_t i = 0; i < sel.size(); ++i) {
+            FileSource src;
+            src.fd = fd;
+            src.path = path;
+            src.count = h.counts[sel[i]];
+            src.planes0 = poff[sel[i]];
+            src.mags0 = src.planes0 + src.count * kp * wpp * 8;
+            src.ids0 = src.mags0 + src.count * 4;
+            src.kp = uint32_t(kp);
+            src.wpp = uint32_t(wpp);
+            src.threads = io_threads ? io_threads : default_io_threads();
+            src.bytes_read = &bytes;
+            try {
+                stream_partition(ix.get(), uint32_t(i), src);
+            } catch (const InvalidArgument& e) {
+                throw InvalidArgument(std::string("rbe_cuda_index_open_rbei: ") + e.what());
+            }
+        }
+        if (stats) {
+            stats->file_bytes_read = bytes;
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        *out = ix.release();
     });
 }
 

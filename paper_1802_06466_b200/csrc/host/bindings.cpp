@@ -114,8 +114,9 @@ PYBIND11_MODULE(_core, m) {
                  const Partition& part = k.partitions.at(p);
                  const size_t wpp = k.words_per_plane();
                  py::array_t<uint64_t> planes({size_t(k.keyword_planes), size_t(part.count * wpp)});
-                 for (uint32_t t = 0; t < k.keyword_planes; ++t)
-                     std::memcpy(planes.mutable_data(t, 0), part.plane_blocks[t].data(), part.count * wpp * 8);
+                 if (part.count)
+                     for (uint32_t t = 0; t < k.keyword_planes; ++t)
+                         std::memcpy(planes.mutable_data(t, 0), part.plane_blocks[t].data(), part.count * wpp * 8);
                  py::array_t<float> mags(part.count);
                  std::memcpy(mags.mutable_data(), part.magnitudes.data(), part.count * 4);
                  py::array_t<uint64_t> ids(part.count);
@@ -182,7 +183,25 @@ PYBIND11_MODULE(_core, m) {
         .def_readonly("device_ms", &SearchStats::device_ms);
 
     // --- the device store
-    py::class_<DeviceIndex, std::shared_ptr<DeviceIndex>>(m, "DeviceIndex")
+    m.def(
+        "rbei_header",
+        [](const std::string& path) {
+            rbe_index_shape shape{};
+            uint32_t P = 0;
+            if (rbe_cuda_rbei_header(path.c_str(), &shape, &P, nullptr, 0) != RBE_CUDA_OK)
+                throw std::runtime_error(rbe_cuda_last_error());
+            std::vector<uint64_t> counts(P);
+            if (rbe_cuda_rbei_header(path.c_str(), &shape, &P, counts.data(), P) != RBE_CUDA_OK)
+                throw std::runtime_error(rbe_cuda_last_error());
+            py::dict d;
+            d["dim"] = shape.dim;
+            d["keyword_planes"] = shape.keyword_planes;
+            d["residual_weights"] = shape.residual_weights != 0;
+            d["counts"] = counts;
+            return d;
+        },
+        py::arg("path"), "RBEI v1 header (host only): shape and partition sizes");
+    py::class_<DeviceIndex, std::shared_ptr<DeviceIndex>>(m, "DeviceIndex", py::dynamic_attr())
         .def(py::init([](const KeywordIndex& k, std::vector<int> devices) {
                  py::gil_scoped_release nogil;
                  return std::make_shared<DeviceIndex>(k, std::move(devices));
@@ -199,6 +218,25 @@ PYBIND11_MODULE(_core, m) {
             py::arg("dim"), py::arg("keyword_planes"), py::arg("residual_weights"), py::arg("n_docs"),
             py::arg("partitions") = 1, py::arg("seed") = 0xD0C5, py::arg("devices") = std::vector<int>{0},
             py::arg("rank") = 0, py::arg("world") = 1)
+        .def_static(
+            "from_rbei",
+            [](const std::string& path, std::vector<int> devices, uint32_t io_threads) {
+                LoadStats st;
+                std::shared_ptr<DeviceIndex> ix;
+                {
+                    py::gil_scoped_release nogil;
+                    ix = std::make_shared<DeviceIndex>(DeviceIndex::from_rbei(path, std::move(devices), io_threads, &st));
+                }
+                py::object o = py::cast(ix);
+                py::dict d;
+                d["file_bytes"] = st.file_bytes;
+                d["seconds"] = st.seconds;
+                d["gb_per_s"] = st.seconds > 0 ? double(st.file_bytes) / st.seconds / 1e9 : 0.0;
+                o.attr("load_stats") = d;
+                return o;
+            },
+            py::arg("path"), py::arg("devices") = std::vector<int>{0}, py::arg("io_threads") = 0,
+            "RBEI file straight into HBM (load_index + upload in one streamed pass); sets .load_stats")
         .def_property_readonly("dim", &DeviceIndex::dim)
         .def_property_readonly("keyword_planes", &DeviceIndex::keyword_planes)
         .def_property_readonly("residual_weights", &DeviceIndex::residual_weights)
@@ -210,6 +248,7 @@ PYBIND11_MODULE(_core, m) {
         .def_property_readonly("devices", &DeviceIndex::devices)
         .def("handle", [](const DeviceIndex& d, size_t i) { return reinterpret_cast<uintptr_t>(d.handle(i)); },
              py::arg("i") = 0)
+        .def("partition_size", &DeviceIndex::partition_size, py::arg("partition"))
         .def("download_partition",
              [](const DeviceIndex& d, uint32_t p) {
                  Partition part;
@@ -219,8 +258,9 @@ PYBIND11_MODULE(_core, m) {
                  }
                  const size_t wpp = PackedBinaryVector::words_for(d.dim());
                  py::array_t<uint64_t> planes({size_t(d.keyword_planes()), size_t(part.count * wpp)});
-                 for (uint32_t t = 0; t < d.keyword_planes(); ++t)
-                     std::memcpy(planes.mutable_data(t, 0), part.plane_blocks[t].data(), part.count * wpp * 8);
+                 if (part.count)
+                     for (uint32_t t = 0; t < d.keyword_planes(); ++t)
+                         std::memcpy(planes.mutable_data(t, 0), part.plane_blocks[t].data(), part.count * wpp * 8);
                  py::array_t<float> mags(part.count);
                  std::memcpy(mags.mutable_data(), part.magnitudes.data(), part.count * 4);
                  py::array_t<uint64_t> ids(part.count);

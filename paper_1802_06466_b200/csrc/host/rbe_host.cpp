@@ -5,6 +5,8 @@
 // include/rbe_cuda.h onto the B200.  Error types and messages follow the
 // reference so callers (and the Python layer) see the same exceptions.
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -373,6 +375,72 @@ DeviceIndex DeviceIndex::synthetic(uint32_t dim, uint32_t kp, bool rw, uint64_t 
             ix.total_ += c;
             ix.max_count_ = std::max(ix.max_count_, c);
         }
+    }
+    return ix;
+}
+
+DeviceIndex DeviceIndex::from_rbei(const std::string& path, std::vector<int> devices, uint32_t io_threads,
+                                   LoadStats* stats) {
+    if (devices.empty()) throw std::invalid_argument("DeviceIndex: need at least one device");
+    const auto t0 = std::chrono::steady_clock::now();
+    rbe_index_shape shape{};
+    uint32_t P = 0;
+    ck(rbe_cuda_rbei_header(path.c_str(), &shape, &P, nullptr, 0));
+    std::vector<uint64_t> counts(P);
+    ck(rbe_cuda_rbei_header(path.c_str(), &shape, &P, counts.data(), P));
+    DeviceIndex ix;
+    ix.devices_ = devices;
+    ix.dim_ = shape.dim;
+    ix.kp_ = shape.keyword_planes;
+    ix.rw_ = shape.residual_weights != 0;
+    ix.partitions_ = P;
+    ix.part_handle_.assign(P, -1);
+    ix.part_local_.assign(P, 0);
+    ix.part_count_.assign(P, 0);
+    const size_t G = devices.size();
+    std::vector<std::vector<uint32_t>> ords(G);
+    for (uint32_t p = 0; p < P; ++p) ords[p % G].push_back(p);
+    // one loader thread per device; the host threads reading the file are split among them
+    const uint32_t per_dev = io_threads ? std::max<uint32_t>(1, io_threads / uint32_t(G))
+                                        : std::max<uint32_t>(1, std::min<uint32_t>(16, std::thread::hardware_concurrency()) /
+                                                                    uint32_t(G));
+    std::vector<rbe_cuda_index*> raw(G, nullptr);
+    std::vector<rbe_load_stats> st(G, rbe_load_stats{0, 0.0});
+    std::vector<int> rc(G, RBE_CUDA_OK);
+    std::vector<std::string> err(G);
+    std::vector<std::thread> pool;
+    for (size_t d = 0; d < G; ++d)
+        pool.emplace_back([&, d] {
+            // a device without partitions gets an empty handle (n = 0 would mean "all partitions")
+            rc[d] = ords[d].empty()
+                        ? rbe_cuda_index_create(&shape, 0, nullptr, nullptr, devices[d], &raw[d])
+                        : rbe_cuda_index_open_rbei(path.c_str(), ords[d].data(), uint32_t(ords[d].size()), devices[d],
+                                                   per_dev, &raw[d], &st[d]);
+            if (rc[d] != RBE_CUDA_OK) err[d] = rbe_cuda_last_error();
+        });
+    for (auto& t : pool) t.join();
+    for (size_t d = 0; d < G; ++d) ix.handles_.emplace_back(raw[d]);  // owned (destroyed on error too)
+    for (size_t d = 0; d < G; ++d)
+        if (rc[d] != RBE_CUDA_OK) {
+            if (rc[d] == RBE_CUDA_EINVAL) throw std::invalid_argument(err[d]);
+            if (rc[d] == RBE_CUDA_ERANGE) throw std::out_of_range(err[d]);
+            throw std::runtime_error(err[d]);
+        }
+    uint64_t bytes = 0;
+    for (size_t d = 0; d < G; ++d) {
+        bytes += st[d].file_bytes_read;
+        for (size_t i = 0; i < ords[d].size(); ++i) {
+            const uint32_t p = ords[d][i];
+            ix.part_handle_[p] = int(d);
+            ix.part_local_[p] = uint32_t(i);
+            ix.part_count_[p] = counts[p];
+            ix.total_ += counts[p];
+            ix.max_count_ = std::max(ix.max_count_, counts[p]);
+        }
+    }
+    if (stats) {
+        stats->file_bytes = bytes;
+        stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     return ix;
 }

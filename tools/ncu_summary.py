@@ -1,5 +1,5 @@
 """Summarise the ncu outputs of tools/profile_tensor.sh into profiles/ (run here):
-python tools/ncu_summary.py TAG  ->  profiles/TAG_ncu_launches.txt, profiles/TAG_ncu_scan.txt,
+python tools/ncu_summary.py TAG [ALGORITHMIC_BYTES_PER_LAUNCH] [CONFIG]  ->  profiles/TAG_ncu_launches.txt, profiles/TAG_ncu_scan.txt,
                                      profiles/scan_traffic.json (dram bytes per main-scan launch)."""
 import collections
 import csv
@@ -53,6 +53,8 @@ def to_bytes(uv):
 
 
 traffic = to_bytes(vals["dram__bytes_read.sum"]) + to_bytes(vals["dram__bytes_write.sum"])
+algo = float(sys.argv[2]) if len(sys.argv) > 2 else 52e9
+config = sys.argv[3] if len(sys.argv) > 3 else "bench default: 1B docs, P=8, Q=64, k=1000 (one launch scans all partitions)"
 json.dump({"dram_bytes_per_launch": traffic, "kernel": "tensor_scan_kernel (main pass)", "source": f"profiles/{tag}_ncu_scan.txt",
-           "algorithmic_bytes_per_launch": 5.2e9}, open("profiles/scan_traffic.json", "w"), indent=1)
+           "algorithmic_bytes_per_launch": algo, "config": config}, open("profiles/scan_traffic.json", "w"), indent=1)
 print("traffic", traffic)
