@@ -78,6 +78,16 @@ public:
     /// load_index (std::runtime_error); magnitudes must be finite and > 0.
     static DeviceIndex from_rbei(const std::string& path, std::vector<int> devices = {0}, uint32_t io_threads = 0,
                                  LoadStats* stats = nullptr);
+    /// RBEE bulk embeddings built into an index on the device(s): the
+    /// reference's `rbe build` loop (EmbeddingReader + IndexBuilder, src/embedding_io.cpp:48-95,
+    /// src/index.cpp:36-78) with the records streamed to HBM, scattered round-robin into the
+    /// partitions and their magnitudes recomputed on the device where not > 0.  Partition p on
+    /// devices[p % devices.size()]; same errors as the reference.
+    static DeviceIndex build_rbee(const std::string& path, uint32_t partitions, std::vector<int> devices = {0},
+                                  uint32_t io_threads = 0, LoadStats* stats = nullptr);
+    /// Write the index as an RBEI v1 file (byte-identical to save_index of the same
+    /// KeywordIndex), one partition at a time from the device.
+    void save_index(const std::string& path) const;
     ~DeviceIndex();
     DeviceIndex(DeviceIndex&&) noexcept;
     DeviceIndex& operator=(DeviceIndex&&) noexcept;

@@ -144,6 +144,26 @@ int rbe_cuda_index_open_rbei(const char* path, const uint32_t* partitions, uint3
                              int device, uint32_t io_threads, rbe_cuda_index** out,
                              rbe_load_stats* stats);
 
+/* RBEE v1 bulk embeddings -> index build on the device.  Replaces
+ * the reference's EmbeddingReader + IndexBuilder loop of `rbe build`
+ * (src/embedding_io.cpp:48-95, src/index.cpp:36-78, tools/rbe_main.cpp:109-123):
+ * record k goes to partition k % n_partitions_total, slot k / n_partitions_total;
+ * a record magnitude that is not > 0 is recomputed on the device exactly as
+ * make_embedding does.  Errors as the reference (header: ERUNTIME "cannot open
+ * embeddings file", "not an RBEE embeddings file", "unsupported embeddings version",
+ * "embeddings file has empty shape", "embeddings file has truncated records"; EINVAL
+ * "IndexBuilder: need at least one partition", "IndexBuilder: keyword has zero
+ * magnitude", "IndexBuilder: duplicate keyword id" among this handle's keywords;
+ * non-finite magnitudes are rejected as well).  The handle holds partitions
+ * `partitions[0..n)` (n = 0: all).  Host-only header reader: rbe_cuda_rbee_header. */
+int rbe_cuda_rbee_header(const char* path, rbe_index_shape* shape, uint64_t* count);
+int rbe_cuda_index_build_rbee(const char* path, uint32_t n_partitions_total, const uint32_t* partitions,
+                              uint32_t n_partitions, int device, uint32_t io_threads,
+                              rbe_cuda_index** out, rbe_load_stats* stats);
+/* Every id of the handle's partitions, ascending, into ids[total] (duplicate checks
+ * across handles). */
+int rbe_cuda_index_sorted_ids(const rbe_cuda_index* index, uint64_t* ids);
+
 /* Fill every local partition on the device with the synthetic corpus of
  * global doc g of n_total, bits from counter-based
  * splitmix64(seed) in plane-major stream order, partition g % n_partitions_total,

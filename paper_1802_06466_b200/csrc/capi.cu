@@ -14,6 +14,9 @@
 //    search_device with stats, last_batch_ms, search_multi) reports it.
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -654,6 +657,50 @@ void stream_partition(rbe_cuda_index* ix, uint32_t i, ChunkSource& src) {
     if (*bad) throw InvalidArgument("keyword magnitudes must be finite and > 0");
 }
 
+// RBEE v1 bulk embeddings header ("RBEE", u32 version, dim, plane count, rw; then fixed-width
+// records of u64 id, plane words, f32 magnitude), read as the reference's EmbeddingReader does
+// (src/embedding_io.cpp:48-77), with the same errors
+struct RbeeHeader {
+    rbe_index_shape shape{};
+    uint64_t count = 0;
+    uint64_t record_bytes = 0;
+};
+constexpr uint64_t kRbeeHeaderBytes = 4 + 4 * 4;
+
+RbeeHeader read_rbee_header(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open embeddings file: " + path);
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[4];
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "RBEE", 4) != 0)
+        throw std::runtime_error("not an RBEE embeddings file: " + path);
+    uint32_t h[4] = {0, 0, 0, 0};
+    const size_t got = std::fread(h, 4, 4, f);
+    if (got < 1 || h[0] != 1) throw std::runtime_error("unsupported embeddings version");
+    RbeeHeader r;
+    r.shape.dim = got >= 2 ? h[1] : 0;
+    r.shape.keyword_planes = got >= 3 ? h[2] : 0;
+    r.shape.residual_weights = got >= 4 && h[3] != 0;
+    if (r.shape.dim == 0 || r.shape.keyword_planes == 0) throw std::runtime_error("embeddings file has empty shape: " + path);
+    struct stat sb;
+    if (::stat(path.c_str(), &sb) != 0) throw std::runtime_error("cannot open embeddings file: " + path);
+    const uint64_t size = uint64_t(sb.st_size);
+    const uint64_t wpp = (uint64_t(r.shape.dim) + 63) / 64;
+    r.record_bytes = 8 + uint64_t(r.shape.keyword_planes) * wpp * 8 + 4;
+    if (size < kRbeeHeaderBytes || (size - kRbeeHeaderBytes) % r.record_bytes != 0)
+        throw std::runtime_error("embeddings file has truncated records: " + path);
+    r.count = (size - kRbeeHeaderBytes) / r.record_bytes;
+    return r;
+}
+
+// ascending sort of u64 keys on the device (build-time validation only; thrust's radix sort)
+void sort_u64(uint64_t* d, uint64_t n, cudaStream_t st) {
+    thrust::sort(thrust::cuda::par.on(st), thrust::device_ptr<uint64_t>(d), thrust::device_ptr<uint64_t>(d) + n);
+}
+
 uint32_t default_io_threads() { return std::max(1u, std::min(16u, std::thread::hardware_concurrency())); }
 
 // RBEI v1 header ("RBEI", u32 version, dim, kp, rw, P, u64 count[P]), read the
@@ -802,6 +849,158 @@ int rbe_cuda_rbei_header(const char* path, rbe_index_shape* shape, uint32_t* n_p
         *n_partitions = uint32_t(h.counts.size());
         if (counts)
             for (uint32_t p = 0; p < std::min<uint32_t>(counts_cap, uint32_t(h.counts.size())); ++p) counts[p] = h.counts[p];
+    });
+}
+
+int rbe_cuda_rbee_header(const char* path, rbe_index_shape* shape, uint64_t* count) {
+    return guarded([&] {
+        if (!path || !shape || !count) throw InvalidArgument("rbe_cuda_rbee_header: null argument");
+        const RbeeHeader h = read_rbee_header(path);
+        *shape = h.shape;
+        *count = h.count;
+    });
+}
+
+int rbe_cuda_index_build_rbee(const char* path, uint32_t n_partitions_total, const uint32_t* partitions,
+                              uint32_t n_partitions, int device, uint32_t io_threads, rbe_cuda_index** out,
+                              rbe_load_stats* stats) {
+    return guarded([&] {
+        if (!path || !out || (n_partitions && !partitions)) throw InvalidArgument("rbe_cuda_index_build_rbee: null argument");
+        if (n_partitions_total == 0) throw InvalidArgument("IndexBuilder: need at least one partition");
+        const auto t0 = std::chrono::steady_clock::now();
+        const RbeeHeader h = read_rbee_header(path);
+        const uint32_t P = n_partitions_total;
+        std::vector<uint32_t> sel;
+        if (n_partitions) sel.assign(partitions, partitions + n_partitions);
+        else
+            for (uint32_t p = 0; p < P; ++p) sel.push_back(p);
+        std::vector<int32_t> local(P, -1);
+        std::vector<uint64_t> counts;
+        for (uint32_t i = 0; i < sel.size(); ++i) {
+            if (sel[i] >= P) throw OutOfRange("rbe_cuda_index_build_rbee: partition out of range");
+            local[sel[i]] = int32_t(i);
+            counts.push_back(sel[i] < h.count ? (h.count - sel[i] + P - 1) / P : 0);  // record k -> k % P
+        }
+        rbe_cuda_index* raw = nullptr;
+        const int rc = rbe_cuda_index_create(&h.shape, uint32_t(sel.size()), sel.data(), counts.data(), device, &raw);
+        if (rc != RBE_CUDA_OK) {
+            const std::string msg = g_last_error;
+            if (rc == RBE_CUDA_EINVAL) throw InvalidArgument(msg);
+            if (rc == RBE_CUDA_ERANGE) throw OutOfRange(msg);
+            throw std::runtime_error(msg);
+        }
+        std::unique_ptr<rbe_cuda_index> ix(raw);
+        const int fd = ::open(path, O_RDONLY);
+        if (fd < 0) throw std::runtime_error("cannot open embeddings file: " + std::string(path));
+        struct Fd {
+            int fd;
+            ~Fd() { ::close(fd); }
+        } fd_guard{fd};
+        ::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
+        DeviceGuard dg(device);
+        std::lock_guard<std::mutex> lk(ix->mu);
+        cudaStream_t st = ix->stream;
+        const uint32_t threads = io_threads ? io_threads : default_io_threads();
+        // records streamed in 64 MB chunks: pread -> page-locked staging -> device -> scatter kernel
+        const uint64_t chunk = std::max<uint64_t>(1, (uint64_t(64) << 20) / h.record_bytes);
+        struct Host {
+            uint8_t* p = nullptr;
+            ~Host() {
+                if (p) cudaFreeHost(p);
+            }
+        } host[2];
+        DevBuf drec[2], dlocal, dbad;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        struct Events {
+            cudaEvent_t* e;
+            ~Events() {
+                for (int k = 0; k < 2; ++k)
+                    if (e[k]) cudaEventDestroy(e[k]);
+            }
+        } ev_guard{ev};
+        const uint64_t nchunk = std::min(chunk, std::max<uint64_t>(h.count, 1));
+        for (int k = 0; k < 2; ++k) {
+            RBE_CK(cudaMallocHost(&host[k].p, nchunk * h.record_bytes));
+            drec[k].ensure(nchunk * h.record_bytes);
+            RBE_CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        }
+        dlocal.ensure(sizeof(int32_t) * P);
+        dbad.ensure(16);  // [0] zero magnitudes, [1] non-finite magnitudes, [2] duplicate ids
+        RBE_CK(cudaMemcpyAsync(dlocal.p, local.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice, st));
+        RBE_CK(cudaMemsetAsync(dbad.p, 0, 16, st));
+        uint64_t bytes = 0, c = 0;
+        for (uint64_t r0 = 0; r0 < h.count; r0 += chunk, ++c) {
+            const int k = int(c & 1);
+            const uint64_t n = std::min(chunk, h.count - r0);
+            if (c >= 2) RBE_CK(cudaEventSynchronize(ev[k]));
+            std::vector<Piece> pcs{Piece{host[k].p, kRbeeHeaderBytes + r0 * h.record_bytes, size_t(n * h.record_bytes)}};
+            const std::string pth(path);
+            run_pieces(pcs, threads, [&](const Piece& pc) {
+                size_t done = 0;
+                while (done < pc.len) {
+                    const ssize_t r = ::pread(fd, pc.dst + done, pc.len - done, off_t(pc.off + done));
+                    if (r < 0 && errno == EINTR) continue;
+                    if (r <= 0) throw std::runtime_error("truncated embeddings record");
+                    done += size_t(r);
+                }
+            });
+            bytes += n * h.record_bytes;
+            RBE_CK(cudaMemcpyAsync(drec[k].p, host[k].p, n * h.record_bytes, cudaMemcpyHostToDevice, st));
+            launch_rbee_scatter(drec[k].as<uint32_t>(), r0, n, P, dlocal.as<int32_t>(), ix->d_parts.as<PartDesc>(),
+                                ix->shape, ix->perm, dbad.as<uint32_t>(), st);
+            RBE_CK(cudaEventRecord(ev[k], st));
+        }
+        // IndexBuilder::finish: duplicate ids (within this handle; across handles the caller merges)
+        uint64_t total = 0;
+        for (auto& L : ix->parts) total += L.count;
+        uint32_t* h_flags = reinterpret_cast<uint32_t*>(ix->host_out);
+        if (total > 1) {
+            DevBuf sorted;
+            sorted.ensure(total * 8);
+            uint64_t off = 0;
+            for (auto& L : ix->parts) {
+                RBE_CK(cudaMemcpyAsync(sorted.as<uint64_t>() + off, L.ids, L.count * 8, cudaMemcpyDeviceToDevice, st));
+                off += L.count;
+            }
+            sort_u64(sorted.as<uint64_t>(), total, st);
+            launch_count_adjacent_equal(sorted.as<uint64_t>(), total, dbad.as<uint32_t>() + 2, st);
+        }
+        RBE_CK(cudaMemcpyAsync(h_flags, dbad.p, 12, cudaMemcpyDeviceToHost, st));
+        RBE_CK(cudaStreamSynchronize(st));
+        ix->mag_range_ok = false;
+        if (h_flags[0]) throw InvalidArgument("IndexBuilder: keyword has zero magnitude");
+        if (h_flags[1]) throw InvalidArgument("rbe_cuda_index_build_rbee: keyword magnitudes must be finite and > 0");
+        if (h_flags[2]) throw InvalidArgument("IndexBuilder: duplicate keyword id");
+        if (stats) {
+            stats->file_bytes_read = bytes;
+            stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        *out = ix.release();
+    });
+}
+
+int rbe_cuda_index_sorted_ids(const rbe_cuda_index* cix, uint64_t* ids) {
+    return guarded([&] {
+        rbe_cuda_index* ix = const_cast<rbe_cuda_index*>(cix);
+        if (!ix || !ids) throw InvalidArgument("rbe_cuda_index_sorted_ids: null argument");
+        std::lock_guard<std::mutex> lk(ix->mu);
+        DeviceGuard dg(ix->device);
+        uint64_t total = 0;
+        for (auto& L : ix->parts) total += L.count;
+        if (!total) return;
+        cudaStream_t st = ix->stream;
+        ix->order.acquire(st);
+        DevBuf sorted;
+        sorted.ensure(total * 8);
+        uint64_t off = 0;
+        for (auto& L : ix->parts) {
+            RBE_CK(cudaMemcpyAsync(sorted.as<uint64_t>() + off, L.ids, L.count * 8, cudaMemcpyDeviceToDevice, st));
+            off += L.count;
+        }
+        sort_u64(sorted.as<uint64_t>(), total, st);
+        RBE_CK(cudaMemcpyAsync(ids, sorted.p, total * 8, cudaMemcpyDeviceToHost, st));
+        ix->order.release(st);
+        RBE_CK(cudaStreamSynchronize(st));
     });
 }
 

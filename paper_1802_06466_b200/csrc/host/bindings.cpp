@@ -201,6 +201,20 @@ PYBIND11_MODULE(_core, m) {
             return d;
         },
         py::arg("path"), "RBEI v1 header (host only): shape and partition sizes");
+    m.def(
+        "rbee_header",
+        [](const std::string& path) {
+            rbe_index_shape shape{};
+            uint64_t n = 0;
+            if (rbe_cuda_rbee_header(path.c_str(), &shape, &n) != RBE_CUDA_OK) throw std::runtime_error(rbe_cuda_last_error());
+            py::dict d;
+            d["dim"] = shape.dim;
+            d["plane_count"] = shape.keyword_planes;
+            d["residual_weights"] = shape.residual_weights != 0;
+            d["count"] = n;
+            return d;
+        },
+        py::arg("path"), "RBEE v1 header (host only): shape and record count");
     py::class_<DeviceIndex, std::shared_ptr<DeviceIndex>>(m, "DeviceIndex", py::dynamic_attr())
         .def(py::init([](const KeywordIndex& k, std::vector<int> devices) {
                  py::gil_scoped_release nogil;
@@ -237,6 +251,34 @@ PYBIND11_MODULE(_core, m) {
             },
             py::arg("path"), py::arg("devices") = std::vector<int>{0}, py::arg("io_threads") = 0,
             "RBEI file straight into HBM (load_index + upload in one streamed pass); sets .load_stats")
+        .def_static(
+            "build_rbee",
+            [](const std::string& path, uint32_t partitions, std::vector<int> devices, uint32_t io_threads) {
+                LoadStats st;
+                std::shared_ptr<DeviceIndex> ix;
+                {
+                    py::gil_scoped_release nogil;
+                    ix = std::make_shared<DeviceIndex>(
+                        DeviceIndex::build_rbee(path, partitions, std::move(devices), io_threads, &st));
+                }
+                py::object o = py::cast(ix);
+                py::dict d;
+                d["file_bytes"] = st.file_bytes;
+                d["seconds"] = st.seconds;
+                d["gb_per_s"] = st.seconds > 0 ? double(st.file_bytes) / st.seconds / 1e9 : 0.0;
+                o.attr("load_stats") = d;
+                return o;
+            },
+            py::arg("path"), py::arg("partitions") = 1, py::arg("devices") = std::vector<int>{0},
+            py::arg("io_threads") = 0,
+            "RBEE bulk embeddings built into an index on the device (rbe build); sets .load_stats")
+        .def(
+            "save_index",
+            [](const DeviceIndex& d, const std::string& path) {
+                py::gil_scoped_release nogil;
+                d.save_index(path);
+            },
+            py::arg("path"))
         .def_property_readonly("dim", &DeviceIndex::dim)
         .def_property_readonly("keyword_planes", &DeviceIndex::keyword_planes)
         .def_property_readonly("residual_weights", &DeviceIndex::residual_weights)

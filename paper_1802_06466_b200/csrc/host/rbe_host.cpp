@@ -445,6 +445,111 @@ DeviceIndex DeviceIndex::from_rbei(const std::string& path, std::vector<int> dev
     return ix;
 }
 
+DeviceIndex DeviceIndex::build_rbee(const std::string& path, uint32_t partitions, std::vector<int> devices,
+                                    uint32_t io_threads, LoadStats* stats) {
+    if (devices.empty()) throw std::invalid_argument("DeviceIndex: need at least one device");
+    if (partitions == 0) throw std::invalid_argument("IndexBuilder: need at least one partition");
+    const auto t0 = std::chrono::steady_clock::now();
+    rbe_index_shape shape{};
+    uint64_t n = 0;
+    ck(rbe_cuda_rbee_header(path.c_str(), &shape, &n));
+    DeviceIndex ix;
+    ix.devices_ = devices;
+    ix.dim_ = shape.dim;
+    ix.kp_ = shape.keyword_planes;
+    ix.rw_ = shape.residual_weights != 0;
+    ix.partitions_ = partitions;
+    ix.part_handle_.assign(partitions, -1);
+    ix.part_local_.assign(partitions, 0);
+    ix.part_count_.assign(partitions, 0);
+    const size_t G = devices.size();
+    std::vector<std::vector<uint32_t>> ords(G);
+    for (uint32_t p = 0; p < partitions; ++p) ords[p % G].push_back(p);
+    const uint32_t per_dev = std::max<uint32_t>(
+        1, (io_threads ? io_threads : std::min<uint32_t>(16, std::thread::hardware_concurrency())) / uint32_t(G));
+    std::vector<rbe_cuda_index*> raw(G, nullptr);
+    std::vector<rbe_load_stats> st(G, rbe_load_stats{0, 0.0});
+    std::vector<int> rc(G, RBE_CUDA_OK);
+    std::vector<std::string> err(G);
+    std::vector<std::thread> pool;
+    for (size_t d = 0; d < G; ++d)
+        pool.emplace_back([&, d] {
+            rc[d] = ords[d].empty()
+                        ? rbe_cuda_index_create(&shape, 0, nullptr, nullptr, devices[d], &raw[d])
+                        : rbe_cuda_index_build_rbee(path.c_str(), partitions, ords[d].data(), uint32_t(ords[d].size()),
+                                                    devices[d], per_dev, &raw[d], &st[d]);
+            if (rc[d] != RBE_CUDA_OK) err[d] = rbe_cuda_last_error();
+        });
+    for (auto& t : pool) t.join();
+    for (size_t d = 0; d < G; ++d) ix.handles_.emplace_back(raw[d]);
+    for (size_t d = 0; d < G; ++d)
+        if (rc[d] != RBE_CUDA_OK) {
+            if (rc[d] == RBE_CUDA_EINVAL) throw std::invalid_argument(err[d]);
+            if (rc[d] == RBE_CUDA_ERANGE) throw std::out_of_range(err[d]);
+            throw std::runtime_error(err[d]);
+        }
+    uint64_t bytes = 0;
+    std::vector<uint64_t> held(G, 0);
+    for (size_t d = 0; d < G; ++d) {
+        bytes = std::max<uint64_t>(bytes, st[d].file_bytes_read);
+        for (size_t i = 0; i < ords[d].size(); ++i) {
+            const uint32_t p = ords[d][i];
+            const uint64_t c = p < n ? (n - p + partitions - 1) / partitions : 0;
+            ix.part_handle_[p] = int(d);
+            ix.part_local_[p] = uint32_t(i);
+            ix.part_count_[p] = c;
+            ix.total_ += c;
+            ix.max_count_ = std::max(ix.max_count_, c);
+            held[d] += c;
+        }
+    }
+    // IndexBuilder::finish across handles: each handle checked its own ids; merge the sorted lists
+    size_t with_ids = 0;
+    for (uint64_t h : held) with_ids += h ? 1 : 0;
+    if (with_ids > 1) {
+        std::vector<uint64_t> all;
+        all.reserve(ix.total_);
+        for (size_t d = 0; d < G; ++d) {
+            if (!held[d]) continue;
+            std::vector<uint64_t> ids(held[d]);
+            ck(rbe_cuda_index_sorted_ids(ix.handles_[d].get(), ids.data()));
+            const size_t mid = all.size();
+            all.insert(all.end(), ids.begin(), ids.end());
+            std::inplace_merge(all.begin(), all.begin() + mid, all.end());
+        }
+        if (std::adjacent_find(all.begin(), all.end()) != all.end())
+            throw std::invalid_argument("IndexBuilder: duplicate keyword id");
+    }
+    if (stats) {
+        stats->file_bytes = bytes;
+        stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return ix;
+}
+
+void DeviceIndex::save_index(const std::string& path) const {
+    for (int h : part_handle_)
+        if (h < 0) throw std::out_of_range("save_index: not every partition is resident in this process");
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot open index for writing: " + path);
+    auto u32 = [&](uint32_t v) { out.write(reinterpret_cast<const char*>(&v), 4); };
+    out.write("RBEI", 4);
+    u32(1);
+    u32(dim_);
+    u32(kp_);
+    u32(rw_ ? 1 : 0);
+    u32(partitions_);
+    for (uint32_t p = 0; p < partitions_; ++p) out.write(reinterpret_cast<const char*>(&part_count_[p]), 8);
+    for (uint32_t p = 0; p < partitions_; ++p) {
+        const Partition part = download_partition(p);
+        for (const auto& blk : part.plane_blocks)
+            out.write(reinterpret_cast<const char*>(blk.data()), std::streamsize(blk.size() * 8));
+        out.write(reinterpret_cast<const char*>(part.magnitudes.data()), std::streamsize(part.count * 4));
+        out.write(reinterpret_cast<const char*>(part.ids.data()), std::streamsize(part.count * 8));
+    }
+    if (!out) throw std::runtime_error("failed writing index: " + path);
+}
+
 uint64_t DeviceIndex::device_bytes() const {
     uint64_t t = 0;
     for (auto& h : handles_) {

@@ -171,6 +171,74 @@ __global__ void fill_synthetic_kernel(uint32_t* __restrict__ planes, float* __re
     }
 }
 
+// RBEE records [rec0, rec0 + n) (raw bytes: u64 id, [kp][wpp] u64 plane words, f32 magnitude;
+// embedding_io.cpp:32-45, records 4-byte aligned in the file, so words are read as u32 halves)
+// -> the store, with IndexBuilder::add's semantics (src/index.cpp:36-78): record k goes to
+// partition k % P, slot k / P, if this handle holds that partition (local[p] >= 0); the
+// magnitude is kept when > 0, else recomputed as make_embedding does (refined_vector over the
+// first dim bits, same IEEE double operation order as fill_synthetic_kernel); a magnitude that
+// is still not > 0 is counted in bad[0] (IndexBuilder: keyword has zero magnitude), a
+// non-finite one in bad[1] (documented deviation: the store requires finite magnitudes).
+__global__ void rbee_scatter_kernel(const uint32_t* __restrict__ rec, uint64_t rec0, uint64_t n, uint32_t P,
+                                    const int32_t* __restrict__ local, const PartDesc* __restrict__ parts,
+                                    uint32_t dim, uint32_t kp, uint32_t wpp, uint32_t rw, PlanePerm perm,
+                                    uint32_t* bad) {
+    const uint32_t w32 = 2 * wpp;
+    const uint64_t rec_words = 3 + uint64_t(kp) * w32;  // u32 words per record
+    for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < n;
+         k += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t g = rec0 + k;
+        const int32_t li = local[g % P];
+        if (li < 0) continue;
+        const PartDesc& part = parts[li];
+        uint32_t* planes = const_cast<uint32_t*>(part.planes);  // the store is ours to fill
+        const uint64_t s = g / P;
+        const uint32_t* r = rec + k * rec_words;
+        const uint64_t id = uint64_t(r[0]) | (uint64_t(r[1]) << 32);
+        const uint32_t* words = r + 2;
+        for (uint32_t t = 0; t < kp; ++t) {
+            const uint8_t* pm = perm.perm[t < uint32_t(kMaxPlanes) ? t : 0];
+            uint32_t* dst = planes + (uint64_t(t) * part.count_pad + s) * w32;
+            for (uint32_t h = 0; h < w32; ++h) dst[h] = permute_word(words[t * w32 + h], pm);
+        }
+        if (interleaved_store(int(kp), rw != 0)) {
+            for (uint32_t h = 0; h < w32; ++h) {
+                uint32_t w[3], z[3];
+                for (uint32_t t = 0; t < 3; ++t) w[t] = planes[(uint64_t(t) * part.count_pad + s) * w32 + h];
+                interleave3(w, z);
+                for (uint32_t t = 0; t < 3; ++t) planes[(uint64_t(t) * part.count_pad + s) * w32 + h] = z[t];
+            }
+        }
+        float m = __uint_as_float(r[2 + kp * w32]);
+        if (!(double(m) > 0.0)) {
+            double sq = 0.0;
+            for (uint32_t w = 0; w < wpp; ++w) {
+                const uint32_t nbits = (w + 1 == wpp && dim % 64) ? dim % 64 : 64;
+                double x[64];
+#pragma unroll
+                for (int b = 0; b < 64; ++b) x[b] = 0.0;
+                for (uint32_t t = 0; t < kp; ++t) {
+                    const uint64_t v = uint64_t(words[t * w32 + 2 * w]) | (uint64_t(words[t * w32 + 2 * w + 1]) << 32);
+                    const double wt = rw ? ldexp(1.0, -int(t)) : 1.0;
+#pragma unroll
+                    for (int b = 0; b < 64; ++b) x[b] = __dadd_rn(x[b], ((v >> b) & 1) ? wt : -wt);
+                }
+                for (uint32_t b = 0; b < nbits; ++b) sq = __dadd_rn(sq, __dmul_rn(x[b], x[b]));
+            }
+            m = __double2float_rn(__dsqrt_rn(sq));
+            if (!(double(m) > 0.0)) atomicAdd(bad, 1u);
+        }
+        if (!isfinite(m)) atomicAdd(bad + 1, 1u);
+        const_cast<float*>(part.mags)[s] = m;
+        const_cast<uint64_t*>(part.ids)[s] = id;
+    }
+}
+
+__global__ void count_adjacent_equal_kernel(const uint64_t* __restrict__ a, uint64_t n, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i + 1 < n; i += uint64_t(gridDim.x) * blockDim.x)
+        if (a[i] == a[i + 1]) atomicAdd(out, 1u);
+}
+
 __global__ void validate_mags_kernel(const float* __restrict__ mags, uint64_t count, uint32_t* bad) {
     for (uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; s < count;
          s += uint64_t(gridDim.x) * blockDim.x) {
@@ -228,6 +296,21 @@ void launch_fill_synthetic(uint32_t* d_planes, float* d_mags, uint64_t* d_ids, u
     fill_synthetic_kernel<<<grid_for(count, 128), 128, 0, st>>>(d_planes, d_mags, d_ids, count, count_pad, ordinal,
                                                                n_parts_total, n_total, seed, s.dim, s.kp, s.wpp,
                                                                s.rw, perm);
+    RBE_CK(cudaGetLastError());
+}
+
+void launch_rbee_scatter(const uint32_t* d_records, uint64_t rec0, uint64_t n, uint32_t P, const int32_t* d_local,
+                         const PartDesc* d_parts, const Shape& s, const PlanePerm& perm, uint32_t* d_bad,
+                         cudaStream_t st) {
+    if (n == 0) return;
+    rbee_scatter_kernel<<<grid_for(n, 128), 128, 0, st>>>(d_records, rec0, n, P, d_local, d_parts, s.dim, s.kp, s.wpp,
+                                                         s.rw, perm, d_bad);
+    RBE_CK(cudaGetLastError());
+}
+
+void launch_count_adjacent_equal(const uint64_t* d_sorted, uint64_t n, uint32_t* d_out, cudaStream_t st) {
+    if (n < 2) return;
+    count_adjacent_equal_kernel<<<grid_for(n), kThreads, 0, st>>>(d_sorted, n, d_out);
     RBE_CK(cudaGetLastError());
 }
 

@@ -50,6 +50,13 @@ void launch_fill_synthetic(uint32_t* d_planes, float* d_mags, uint64_t* d_ids, u
                            uint64_t count_pad, uint32_t ordinal, uint32_t n_parts_total, uint64_t n_total,
                            uint64_t seed, const Shape& s, const PlanePerm& perm, cudaStream_t st);
 void launch_validate_mags(const float* d_mags, uint64_t count, uint32_t* d_bad, cudaStream_t st);
+// d_out[0] += number of i with sorted[i] == sorted[i + 1]
+void launch_count_adjacent_equal(const uint64_t* d_sorted, uint64_t n, uint32_t* d_out, cudaStream_t st);
+// RBEE records (raw, 4-byte aligned) -> the partitions of a handle (IndexBuilder::add semantics);
+// d_bad[0]: magnitudes still not > 0 after the recompute, d_bad[1]: non-finite magnitudes
+void launch_rbee_scatter(const uint32_t* d_records, uint64_t rec0, uint64_t n, uint32_t P, const int32_t* d_local,
+                         const PartDesc* d_parts, const Shape& s, const PlanePerm& perm, uint32_t* d_bad,
+                         cudaStream_t st);
 void launch_fill_f32(float* p, uint64_t n, float v, cudaStream_t st);
 // d_out[0] = min, d_out[1] = max magnitude bits (caller initialises to ~0u / 0)
 void launch_mag_range(const float* d_mags, uint64_t count, uint32_t* d_out, cudaStream_t st);

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--dir", default="/tmp")
     ap.add_argument("--io-threads", type=int, default=0)
     ap.add_argument("--skip-host-path", action="store_true")
+    ap.add_argument("--rbee", action="store_true", help="also time the RBEE -> device index build")
     args = ap.parse_args()
     import paper_1802_06466_b200 as rbe
 
@@ -82,6 +83,36 @@ def main():
                                          "gb_per_s": round(size / (t_load + t_up) / 1e9, 2)}
         del dix, host
     os.remove(path)
+    if args.rbee:
+        # RBEE bulk embeddings (magnitudes 0: every one recomputed on the device) -> build_rbee
+        rpath = os.path.join(args.dir, f"ingest_{args.docs}.rbee")
+        src = rbe.DeviceIndex.synthetic(dim, kp, True, args.docs, 1, 0xD0C5, [0])
+        planes, _, ids = src.download_partition(0)
+        del src
+        n = args.docs
+        rec = np.zeros(n, dtype=[("id", "<u8"), ("w", "<u8", (kp * 2,)), ("m", "<f4")])
+        rec["id"] = ids
+        rec["w"] = np.asarray(planes).reshape(kp, n, 2).transpose(1, 0, 2).reshape(n, kp * 2)
+        with open(rpath, "wb") as f:
+            f.write(b"RBEE" + struct.pack("<4I", 1, dim, kp, 1))
+            rec.tofile(f)
+        del rec, planes, ids
+        dix = rbe.DeviceIndex.build_rbee(rpath, P, [0], args.io_threads)
+        st = dix.load_stats
+        out["build_rbee_warm"] = {"seconds": round(st["seconds"], 3), "gb_per_s": round(st["gb_per_s"], 2),
+                                  "docs_per_s": round(n / st["seconds"])}
+        del dix
+        # the reference's IndexBuilder (make_embedding per keyword) on a 1M-doc sample, 1 thread
+        from oracle.oracle import Port, Ref
+
+        m = min(n, 1_000_000)
+        w = Port().gen_partition_prefix(0xD0C5, m, dim, kp, 1, 0, m, 16)[0]
+        words = np.asarray(w).reshape(kp, m, 2).transpose(1, 0, 2).copy()
+        t = time.perf_counter()
+        Ref().build_index(dim, kp, True, P, words, np.arange(m, dtype=np.uint64))
+        dt = time.perf_counter() - t
+        out["reference_index_builder_1thread"] = {"sample_docs": m, "seconds": round(dt, 3), "docs_per_s": round(m / dt)}
+        os.remove(rpath)
     print(json.dumps(out))
 
 
