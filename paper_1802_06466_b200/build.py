@@ -5,6 +5,7 @@ travel to the GPU box with the repo snapshot):
                         (nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo)
   _lib/librbe.so        host C++ rbe:: API (include/rbe/*.hpp) over the C ABI
   _lib/_core*.so        pybind11 module (drop-in for the reference's rbe._core)
+  _lib/rbe-cuda         command-line caller (build / query subcommands of the reference CLI)
 
 Usage: python -m paper_1802_06466_b200.build [--force]
 """
@@ -86,6 +87,11 @@ def build(force: bool = False, verbose: bool = False) -> dict:
         _run(["g++"] + CXX_FLAGS + ["-shared", "-o", core_so, bind_src, f"-I{pybind11.get_include()}",
                                     f"-I{sysconfig.get_paths()['include']}", f"-L{LIB}", "-lrbe", "-lrbe_cuda",
                                     "-Wl,-rpath,$ORIGIN"])
+    cli_src = os.path.join(CSRC, "host", "cli.cpp")
+    cli_bin = os.path.join(LIB, "rbe-cuda")
+    if force or _newer(cli_bin, [cli_src, rbe_so] + host_hdrs + hdrs):
+        _run(["g++"] + [f for f in CXX_FLAGS if f != "-fPIC"] + ["-o", cli_bin, cli_src, f"-L{LIB}", "-lrbe",
+                                                                   "-lrbe_cuda", "-Wl,-rpath,$ORIGIN"])
     init = os.path.join(LIB, "__init__.py")
     if not os.path.exists(init):
         open(init, "w").close()
@@ -94,7 +100,7 @@ def build(force: bool = False, verbose: bool = False) -> dict:
             log = o + ".ptxas.log"
             if os.path.exists(log):
                 print(open(log).read())
-    return {"librbe_cuda": cuda_so, "librbe": rbe_so, "core": core_so}
+    return {"librbe_cuda": cuda_so, "librbe": rbe_so, "core": core_so, "cli": cli_bin}
 
 
 if __name__ == "__main__":
