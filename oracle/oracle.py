@@ -167,6 +167,13 @@ class Ref:
                                          C.byref(out)))
         return out.value
 
+    def expected_recall(self, candidates, relevant, items_per_thread):
+        """Appendix A prediction (src/analysis.cpp:143-184): (recall@N, expected misses)."""
+        r, m = C.c_double(), C.c_double()
+        self._check(self.L.ref_expected_recall(C.c_uint64(candidates), C.c_uint64(relevant),
+                                               C.c_uint64(items_per_thread), C.byref(r), C.byref(m)))
+        return r.value, m.value
+
     def thread_assignment(self, geometry, count, block, thread):
         b, t, i, q = geometry
         out = np.zeros(max(i, 1), dtype=np.uint64)

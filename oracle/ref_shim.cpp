@@ -18,6 +18,7 @@
 #include "rbe/binary_vector.hpp"
 #include "rbe/embedding.hpp"
 #include "rbe/index.hpp"
+#include "rbe/analysis.hpp"
 #include "rbe/search.hpp"
 
 namespace {
@@ -332,6 +333,26 @@ int ref_scan_benchmark(uint64_t count, uint32_t dim, uint32_t qp, uint32_t kp, u
         rbe::BenchResult r = rbe::run_scan_benchmark(count, dim, qp, kp, repeats, seed, true, true);
         *binary_tput = r.binary_throughput;
         *float_tput = r.float_throughput;
+    })
+}
+
+// Appendix A selection-miss model (src/analysis.cpp:143-184): predicted recall@N of the
+// length-1-queue scan of C candidates with I items per thread.
+int ref_expected_recall(uint64_t C, uint64_t N, uint64_t I, double* recall, double* misses) {
+    REF_TRY({
+        const rbe::RecallPrediction r = rbe::expected_recall(C, N, I);
+        *recall = r.expected_recall;
+        *misses = r.expected_misses;
+    })
+}
+
+// Monte Carlo of the same model (src/analysis.cpp:99-141): frequency of L = 0 misses.
+int ref_simulate_miss_zero(uint64_t C, uint64_t N, uint64_t I, uint32_t queue_length, uint64_t trials, uint64_t seed,
+                           double* p_zero) {
+    REF_TRY({
+        const auto f = rbe::simulate_miss(C, N, I, queue_length, trials, seed);
+        auto it = f.find(0);
+        *p_zero = it == f.end() ? 0.0 : it->second;
     })
 }
 
