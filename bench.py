@@ -169,7 +169,8 @@ def cpu_reference(args, steps, warmup, as_shipped=True):
     from oracle.oracle import Port, Ref, gen_queries
 
     threads = os.cpu_count() or 1
-    S = min(args.sample_docs, part_count(args.docs, args.partitions, 0))
+    full = part_count(args.docs, args.partitions, 0)
+    S = min(args.sample_docs, full) if args.sample_docs else full
     ref = Ref()
     planes, mags, ids = Port().gen_partition_prefix(SEED_DOCS, args.docs, DIM, KP, args.partitions, 0, S, threads)
     ix = ref.index(DIM, KP, True, [(planes, mags, ids)])
@@ -187,8 +188,10 @@ def cpu_reference(args, steps, warmup, as_shipped=True):
     per_step = statistics.median(times)
     qps = qs.shape[0] / per_step * scale
     info = {"value": qps, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{qs.shape[0]} queries per step (one per host thread, query-parallel rbe::search) over the "
-                      f"first {S:,} slots of partition 0 of the {args.docs:,}-doc corpus ({S * BYTES_PER_DOC / 1e9:.2f} "
+            "sample": f"{qs.shape[0]} queries per step (one per host thread, query-parallel rbe::search) over "
+                      + (f"all {S:,} slots of partition 0, one of the {args.partitions} equal partitions"
+                         if S == full else f"the first {S:,} slots of partition 0")
+                      + f" of the {args.docs:,}-doc corpus ({S * BYTES_PER_DOC / 1e9:.2f} "
                       f"GB, >> LLC), scaled x{scale:g} to the whole corpus; {len(times)} steps, median "
                       f"{per_step * 1e3:.0f} ms wall / {statistics.median(cpu_times) * 1e3:.0f} ms process CPU per step; "
                       f"reference sources compiled unmodified (oracle/_ref); host {host_cpu()}",
@@ -210,7 +213,7 @@ def cpu_reference(args, steps, warmup, as_shipped=True):
                 pix = ref.index(DIM, KP, True, pparts)
             pgeo = (-(-(-(-S // P)) // 65536), 256, 256, 1)
             t0, c0 = time.perf_counter(), time.process_time()
-            nq = 2
+            nq = 1
             for q in range(nq):
                 pix.search(qs[q:q + 1], pgeo, args.k, threads=1)
             dt, dc = time.perf_counter() - t0, time.process_time() - c0
@@ -399,6 +402,32 @@ def run_ours(args):
                "api": "per rank: H2D query words -> rbe_cuda_search_device; NCCL gather; rbe_cuda_merge_device; "
                       "D2H of the merged records on rank 0"}
 
+    # C4 latency / throughput of the query batch size (Q in [1, 256]) on the
+    # same corpus: device time per batch through the same call (CUDA events on the stream)
+    sweep = None
+    if world == 1 and has_docs and not args.no_q_sweep:
+        sweep = []
+        for nq in (1, 8, 16, 64, 128, 256):
+            qw = gen_queries(SEED_QUERIES + nq, nq, DIM, QP)
+            dw = torch.from_numpy(qw.view(np.int64).copy()).to(dev)
+            ob = torch.empty(nq * K * RESULT_BYTES, dtype=torch.uint8, device=dev)
+            for _ in range(2):
+                rbe.search_device(dix.handle(0), dw.data_ptr(), nq, QP, geo, K, ob.data_ptr(), stream.cuda_stream,
+                                  args.variant, False)
+            reps = 5
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+            evs[0].record(stream)
+            for r in range(reps):
+                rbe.search_device(dix.handle(0), dw.data_ptr(), nq, QP, geo, K, ob.data_ptr(), stream.cuda_stream,
+                                  args.variant, False)
+                evs[r + 1].record(stream)
+            torch.cuda.synchronize()
+            b = [evs[r].elapsed_time(evs[r + 1]) for r in range(reps)]
+            sweep.append({"queries": nq, "batch_ms_p50": statistics.median(b),
+                          "queries_per_s": nq / (statistics.median(b) / 1e3),
+                          "scan_passes": -(-nq // 64)})
+        rbe.last_batch_ms(dix.handle(0))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -426,7 +455,7 @@ def run_ours(args):
                          "aggregate_frac": (args.docs * BYTES_PER_DOC / (ms_per_step / 1e3) / 1e9) / (peak * world)},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
-            "result_sha256": digest, "result_entries": n_valid,
+            "result_sha256": digest, "result_entries": n_valid, "q_sweep": sweep,
             "doc_queries_per_s": value * args.docs,
             "index_build_s": build_s,
             "candidates_per_batch": statistics.mean(s["candidates"] for s in stats) if stats else None,
@@ -450,8 +479,10 @@ def main():
     ap.add_argument("--partitions", type=int, default=8)
     ap.add_argument("--queries", type=int, default=64)
     ap.add_argument("--k", type=int, default=1000)
-    ap.add_argument("--sample-docs", type=int, default=8_000_000)
+    ap.add_argument("--sample-docs", type=int, default=0,
+                    help="CPU reference sample: the first N slots of partition 0 (0 = the whole partition)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-q-sweep", action="store_true", help="skip the C4 query-batch sweep table")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

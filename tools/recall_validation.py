@@ -2,7 +2,11 @@
 PAPER.md:327-329 reports 99.99% recall@1000 over 1.2B keywords).  Validation tool: the
 prediction comes from the reference's own analysis code (oracle/_ref).  Prints one JSON line.
 
-    python tools/recall_validation.py --docs 1000000000 --partitions 8 --queries 64 --n 1000
+    python tools/recall_validation.py --docs 100000000 --partitions 1 --queries 16 --n 1000
+
+The lossless ground truth (one item per logical thread) keeps a survivor slot per document and
+query, so the measured scale is bounded by device memory (C x Q x 32 B); the prediction at
+the headline scale (C = 1B) is printed alongside.
 """
 import argparse
 import json
@@ -17,9 +21,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--docs", type=int, default=1_000_000_000)
-    ap.add_argument("--partitions", type=int, default=8)
-    ap.add_argument("--queries", type=int, default=64)
+    ap.add_argument("--docs", type=int, default=100_000_000)
+    ap.add_argument("--partitions", type=int, default=1)
+    ap.add_argument("--queries", type=int, default=16)
     ap.add_argument("--n", type=int, default=1000)
     ap.add_argument("--items-per-thread", type=int, default=256)
     args = ap.parse_args()
@@ -44,10 +48,11 @@ def main():
     t_lossy = time.perf_counter() - t
     rec = [len(set(exact[q].tolist()) & set(lossy[q].tolist())) / args.n for q in range(args.queries)]
     want, misses = Ref().expected_recall(args.docs, args.n, args.items_per_thread)
+    want_1b, _ = Ref().expected_recall(1_000_000_000, args.n, args.items_per_thread)
     print(json.dumps({"docs": args.docs, "partitions": args.partitions, "queries": args.queries, "n": args.n,
                       "items_per_thread": args.items_per_thread, "measured_recall_mean": float(np.mean(rec)),
                       "measured_recall_min": float(np.min(rec)), "predicted_recall_appendix_a": want,
-                      "predicted_misses": misses, "paper_recall_at_1000": 0.9999,
+                      "predicted_misses": misses, "predicted_recall_at_1B": want_1b, "paper_recall_at_1000_1p2B": 0.9999,
                       "lossless_pass_s": round(t_exact, 3), "lossy_pass_s": round(t_lossy, 3)}))
 
 
