@@ -643,7 +643,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
         theta_s[q] = (live && !PROBE) ? p.theta[p.q0 + q] : INFINITY;
         XCoef x;
         if (PROBE) x = live ? XCoef{int32_t(cq_s[q] * int32_t(1u << p.lam_shift)), 0, 0} : XCoef{-kXMax, 0, 0};
-        else x = x_coeffs(theta_s[q], cq_s[q], L, lam, p.m0, p.delta, p.mmax);
+        // a padding column (q >= nq) has an all-zero query row, so its F is exactly c: -1 keeps the
+        // sign bit of the packed 16-bit epilogue set (c = -kXMax would wrap and flag every doc)
+        else x = live ? x_coeffs(theta_s[q], cq_s[q], L, lam, p.m0, p.delta, p.mmax) : XCoef{-1, 0, 0};
         for (int b = 0; b < 2; ++b) {
             xcoef[(b * 3 + 0) * kQPass + q] = x.c;
             xcoef[(b * 3 + 1) * kQPass + q] = x.e;

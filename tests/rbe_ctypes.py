@@ -27,6 +27,10 @@ class Stats(C.Structure):  # rbe_search_stats
                 ("total_ms", C.c_double), ("launches", C.c_uint32), ("reserved", C.c_uint32 * 3)]
 
 
+class LoadStats(C.Structure):  # rbe_load_stats
+    _fields_ = [("file_bytes_read", C.c_uint64), ("seconds", C.c_double)]
+
+
 def _ptr(t):
     return np.ctypeslib.ndpointer(dtype=t, flags="C_CONTIGUOUS")
 
@@ -51,6 +55,11 @@ def load(path=LIB_PATH):
     lib.rbe_cuda_search.argtypes = [vp, _ptr(np.uint64), u32, u32, C.POINTER(Geometry), u64, vp,
                                     _ptr(np.float64), _ptr(np.uint64), _ptr(np.uint32), _ptr(np.int64),
                                     _ptr(np.uint64), C.POINTER(Stats)]
+    # RBEI v1 straight into HBM (replaces load_index + upload, reference src/index.cpp:170-208)
+    lib.rbe_cuda_rbei_header.restype = i32
+    lib.rbe_cuda_rbei_header.argtypes = [C.c_char_p, C.POINTER(Shape), C.POINTER(u32), _ptr(np.uint64), u32]
+    lib.rbe_cuda_index_open_rbei.restype = i32
+    lib.rbe_cuda_index_open_rbei.argtypes = [C.c_char_p, vp, u32, i32, u32, C.POINTER(vp), C.POINTER(LoadStats)]
     return lib
 
 
@@ -69,6 +78,20 @@ class Index:
             self._ck(lib.rbe_cuda_index_upload_partition(
                 self.h, i, np.ascontiguousarray(planes, np.uint64).reshape(-1), np.ascontiguousarray(mags, np.float32),
                 np.ascontiguousarray(ids, np.uint64)))
+
+    @classmethod
+    def open_rbei(cls, lib, path, device=0):
+        """The whole RBEI file on one device (rbe_cuda_index_open_rbei, partitions = all)."""
+        self = cls.__new__(cls)
+        self.lib = lib
+        shape, P = Shape(), C.c_uint32()
+        self._ck(lib.rbe_cuda_rbei_header(str(path).encode(), C.byref(shape), C.byref(P), np.zeros(1, np.uint64), 0))
+        self.dim = shape.dim
+        self.h = C.c_void_p()
+        self.stats = LoadStats()
+        self._ck(lib.rbe_cuda_index_open_rbei(str(path).encode(), None, 0, device, 0, C.byref(self.h),
+                                              C.byref(self.stats)))
+        return self
 
     def _ck(self, rc):
         if rc != 0:

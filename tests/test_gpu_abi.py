@@ -33,3 +33,20 @@ def test_ctypes_binding_matches_reference(ref, port):
     with pytest.raises(IndexError):
         ix._ck(lib.rbe_cuda_index_upload_partition(ix.h, 7, parts[0][0].reshape(-1), parts[0][1], parts[0][2]))
     ix.close()
+
+
+def test_ctypes_open_rbei_matches_reference(ref, port, tmp_path):
+    """rbe_cuda_index_open_rbei through ctypes on a file the reference wrote (save_index)."""
+    lib = rbe_ctypes.load()
+    dim, kp, qp, P, N, n = 128, 3, 3, 2, 100_003, 100
+    parts = synthetic_partitions(63, N, dim, kp, P, True, port)
+    r = ref.index(dim, kp, True, parts)
+    r.save(tmp_path / "ix.rbei")
+    ix = rbe_ctypes.Index.open_rbei(lib, tmp_path / "ix.rbei")
+    assert ix.stats.file_bytes_read == N * (kp * 2 * 8 + 12)
+    qs = gen_queries(64, 4, dim, qp)
+    geo = (1, 256, 256, 1)
+    got, _ = ix.search(qs, geo, n)
+    want, _ = r.search(qs, geo, n)
+    assert got == want
+    ix.close()
