@@ -370,6 +370,7 @@ Pending enqueue_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t 
     a.mag_hi = ix->mag_hi;
 
     RBE_CK(cudaEventRecord(ix->ev[0], st));
+    uint64_t lossless_cap = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         RBE_CK(cudaMemsetAsync(ix->counters.p, 0, 64, st));
         ix->surv_count.ensure(sizeof(unsigned long long) * Q);
@@ -401,7 +402,7 @@ Pending enqueue_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t 
         }
         std::vector<uint64_t> counts;
         for (auto& p : ix->parts) counts.push_back(p.count);
-        TensorScanPlan plan = plan_tensor_scan(s, qp, *g, Q, counts, n, probe_tiles);
+        TensorScanPlan plan = plan_tensor_scan(s, qp, *g, Q, counts, n, probe_tiles, lossless_cap);
         a.surv_cap = plan.surv_cap;
         ix->surv.ensure(sizeof(Result) * a.surv_cap * Q);
         a.surv = ix->surv.as<Result>();
@@ -413,7 +414,23 @@ Pending enqueue_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t 
         pd.stats.launches += run_tensor_scan(plan, a, s, ix->queries.as<uint64_t>(), ix->qtensor.p, ix->probe.p,
                                              ix->thresholds.p, ix->queue_scratch.p, d_cands, st);
         RBE_CK(cudaEventRecord(ix->ev[2], st));
-        break;  // the tensor kernel emits at most one survivor per logical thread: never overflows
+        // queue_length 1: at most one survivor per logical thread, never overflows.  Lossless
+        // geometry: every document >= theta survives; a bounded list, re-run once with the exact
+        // size if a query overflowed it (synchronous, this case only)
+        if (plan.lossless) {
+            unsigned long long* h = reinterpret_cast<unsigned long long*>(ix->host_out);
+            ix->ensure_host_out(sizeof(unsigned long long) * Q);
+            h = reinterpret_cast<unsigned long long*>(ix->host_out);
+            RBE_CK(cudaMemcpyAsync(h, a.surv_count, sizeof(unsigned long long) * Q, cudaMemcpyDeviceToHost, st));
+            RBE_CK(cudaStreamSynchronize(st));
+            const unsigned long long mx = *std::max_element(h, h + Q);
+            if (mx > plan.surv_cap && attempt == 0) {
+                lossless_cap = mx;
+                continue;
+            }
+            if (mx > plan.surv_cap) throw std::logic_error("tensor scan overflowed its survivor list twice");
+        }
+        break;
     }
     const size_t ss = select_scratch_bytes(Q, a.surv_cap, n);
     ix->sel_scratch.ensure(ss);

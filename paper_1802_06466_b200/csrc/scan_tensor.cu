@@ -123,6 +123,8 @@ struct TensorParams {
     const double* theta0;          // [Q] probe theta (bin 0 lower edge)
     uint64_t n;                    // top-n
     unsigned long long* prof;      // optional [grid][8] phase cycle counters (RBE_PROF=1)
+    uint32_t lossless;             // queue_length >= items_per_thread: every item survives its logical
+                                   // thread, so pairs >= theta are emitted directly (no per-thread state)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -568,6 +570,39 @@ __device__ __noinline__ void take_pair(int32_t F, uint32_t q, uint32_t i, uint32
     take_candidate(a, q, mag, i, col, sw, theta_s, st_key, mags_y, tpb, L, touched, tcount);
 }
 
+// Lossless geometry (queue_length >= items_per_thread): BoundedQueue keeps every item of a
+// logical thread (search.cpp:32-48), so local_select + global_select reduce to the top n of all
+// items under (score desc, id asc).  A passing pair (F >= 0) with its exact score >= theta_q is
+// emitted straight into the survivor list; the histogram of emitted (distinct) documents
+// refines theta exactly as for per-thread survivors.
+__device__ __noinline__ void emit_pair(const TensorParams& p, int32_t F, uint32_t q, uint32_t i, uint32_t col,
+                                       const PartDesc& part, uint64_t base, const int32_t* xc, int32_t cq,
+                                       const double* theta_s) {
+    const uint64_t slot = base + col + uint64_t(i) * p.tpb;
+    const float mag = __ldg(part.mags + slot);
+    const uint32_t j = mag_bin(mag, p.m0f, p.inv_df);
+    const int32_t X = xc[q] - xc[kQPass + q] * int32_t(j) - xc[2 * kQPass + q] * int32_t(j >> 4);
+    const int32_t num = F - X;
+    if (num & ((1 << p.lam_shift) - 1)) atomicAdd(p.error, 1u);
+    const int32_t a = (num >> p.lam_shift) + cq;
+    const double sc = __ddiv_rn(ldexp(double(a), -int(p.L)), double(mag));
+    if (!(sc >= theta_s[q])) return;
+    const unsigned long long pos = atomicAdd(p.surv_count + p.q0 + q, 1ull);
+    if (pos < p.surv_cap) {
+        Result r;
+        r.score = sc;
+        r.id = part.ids[slot];
+        r.acc = a;
+        r.partition = part.ordinal;
+        r.valid = 1;
+        p.surv[uint64_t(p.q0 + q) * p.surv_cap + pos] = r;
+    }
+    const double dq = p.delta_h[p.q0 + q];
+    double fb = floor((sc - p.theta0[p.q0 + q]) / dq);
+    fb = fb < 0.0 ? 0.0 : (fb > double(kBins - 1) ? double(kBins - 1) : fb);
+    atomicAdd(p.hist + uint64_t(p.q0 + q) * kBins + int(fb), 1u);
+}
+
 // Warp roles (17 warps, 120 registers each):
 //   warps 0..4*nwg-1   workers: warpgroup w = warp/4 takes sub-tiles u = w (mod nwg)
 //                      (128 docs, CTA-local counter u); quadrant warp%4 = TMEM lanes.
@@ -974,6 +1009,10 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                                         cqueue[pos] = make_uint2((q << 26) | i, (col << 24) | uint32_t(v[e2]));
                                     else {
                                         const StripInfo si = strip_info(p, s);
+                                        if (p.lossless)
+                                            emit_pair(p, v[e2], q, i, col, p.parts[si.part], si.base,
+                                                      xcoef + xpar * 3 * kQPass, cq_s[q], theta_s);
+                                        else
                                         take_pair(v[e2], q, i, col, p.parts[si.part].mags + si.base + col,
                                                   xcoef + xpar * 3 * kQPass, cq_s[q], p.m0f, p.inv_df, p.lam_shift,
                                                   p.error, sw, theta_s, st_key, p.tpb, L, touched, tcount);
@@ -1073,6 +1112,10 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 for (uint32_t k2 = wt; k2 < nc; k2 += n_workers) {
                     const uint2 c = cqueue[k2];
                     const uint32_t q = c.x >> 26, ii = c.x & 0x3ffffffu, cc = c.y >> 24;
+                    if (p.lossless)
+                        emit_pair(p, int32_t(c.y & 0xffffffu), q, ii, cc, part, si.base, xcoef + (sidx & 1) * 3 * kQPass,
+                                  cq_s[q], theta_s);
+                    else
                     take_pair(int32_t(c.y & 0xffffffu), q, ii, cc, part.mags + si.base + cc,
                               xcoef + (sidx & 1) * 3 * kQPass, cq_s[q], p.m0f, p.inv_df, p.lam_shift, p.error, sw,
                               theta_s, st_key, p.tpb, L, touched, tcount);
@@ -1441,7 +1484,8 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
         if (why) *why = m;
         return false;
     };
-    if (g.queue_length != 1) return no("queue_length != 1");
+    if (g.queue_length != 1 && g.queue_length < g.items_per_thread)
+        return no("1 < queue_length < items_per_thread (partially lossy queues)");
     if (g.threads_per_block % 128 != 0 || g.threads_per_block == 0) return no("threads_per_block not a multiple of 128");
     if (s.kp > 8) return no("more than 8 keyword planes");
     if (s.rw ? qp > 6 : qp > 63) return no("query planes exceed the s8 operand range");
@@ -1460,7 +1504,7 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
 }
 
 TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, uint32_t Q,
-                                const std::vector<uint64_t>& counts, uint64_t n, uint32_t probe_tiles) {
+                                const std::vector<uint64_t>& counts, uint64_t n, uint32_t probe_tiles, uint64_t min_cap) {
     TensorScanPlan pl;
     pl.Q = Q;
     pl.qp = qp;
@@ -1468,9 +1512,16 @@ TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geom
     pl.probe_tiles = probe_tiles ? probe_tiles : 8;
     pl.prefix.assign(counts.size() + 1, 0);
     const uint64_t threads = uint64_t(g.blocks) * g.threads_per_block;
+    uint64_t total = 0;
     for (size_t i = 0; i < counts.size(); ++i) {
         pl.prefix[i + 1] = pl.prefix[i] + count_strips(g, counts[i]);
         pl.surv_cap += std::min<uint64_t>(counts[i], threads);
+        total += counts[i];
+    }
+    pl.lossless = g.queue_length > 1;  // tensor_supported: queue_length == 1 or >= items_per_thread
+    if (pl.lossless) {
+        // every document >= theta is a survivor: a bounded list, grown by the caller on overflow
+        pl.surv_cap = std::min<uint64_t>(total, std::max<uint64_t>({min_cap, 8 * n, uint64_t(1) << 16}));
     }
     pl.surv_cap = std::max<uint64_t>(pl.surv_cap, 1);
     pl.n_strips = pl.prefix.back();
@@ -1559,6 +1610,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     tp.delta_h = delta_h;
     tp.theta0 = theta0;
     tp.n = plan.n;
+    tp.lossless = plan.lossless ? 1u : 0u;
     if (n_strips == 0) return launches;
     const int grid = int(std::min<uint64_t>(n_strips, uint64_t(sm_count())));
 #ifdef RBE_PHASE_PROF
