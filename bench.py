@@ -439,6 +439,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "p50_ms": statistics.median(per),
+            "p99_ms": sorted(per)[max(0, -(-99 * len(per) // 100) - 1)],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "s8xu8->s32 tensor / u32 popc->s64; f64 scores" if stats and stats[0]["variant"] == "tensor"
             else "u32 popc -> s64 acc, f64 score",

@@ -14,6 +14,7 @@
 //    search_device with stats, last_batch_ms, search_multi) reports it.
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/sort.h>
@@ -112,6 +113,13 @@ public:
 };
 
 uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+// NVTX range for the host-side phases (batch enqueue, scan plan, selection, ingest), so a
+// profiler timeline attributes launches to the phase that issued them
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
     int prev = -1;
@@ -324,6 +332,7 @@ struct Pending {
 // acquired ix->order on st and releases it afterwards.
 Pending enqueue_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t qp, const rbe_scan_geometry* g,
                       uint64_t n, const rbe_search_options* opt) {
+    NvtxRange nvtx("rbe_cuda.batch");
     const Shape& s = ix->shape;
     ScanArgs a;
     a.parts = ix->d_parts.as<PartDesc>();
@@ -435,7 +444,10 @@ Pending enqueue_batch(rbe_cuda_index* ix, cudaStream_t st, uint32_t Q, uint32_t 
     const size_t ss = select_scratch_bytes(Q, a.surv_cap, n);
     ix->sel_scratch.ensure(ss);
     ix->out.ensure(sizeof(Result) * size_t(Q) * n);
-    launch_select_topn(a.surv, a.surv_count, a.surv_cap, Q, n, ix->out.as<Result>(), ix->sel_scratch.p, ss, st);
+    {
+        NvtxRange nvtx_sel("rbe_cuda.select");
+        launch_select_topn(a.surv, a.surv_count, a.surv_cap, Q, n, ix->out.as<Result>(), ix->sel_scratch.p, ss, st);
+    }
     pd.stats.launches += 1;
     RBE_CK(cudaEventRecord(ix->ev[3], st));
     pd.surv_cap = a.surv_cap;
@@ -623,6 +635,7 @@ struct FileSource : ChunkSource {
 };
 
 void stream_partition(rbe_cuda_index* ix, uint32_t i, ChunkSource& src) {
+    NvtxRange nvtx("rbe_cuda.ingest_partition");
     auto& L = ix->parts[i];
     if (L.count == 0) return;
     const Shape& s = ix->shape;

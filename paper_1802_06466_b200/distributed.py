@@ -46,58 +46,3 @@ def gather_and_merge(local_results, rank: int, world: int, merge: Callable, dist
         return merge(bufs)
     dist.gather(local_results, gather_list=None, dst=dst)
     return None
-
-
-class ShardedSearcher:
-    """Device-side sharded search for one rank (CUDA/NCCL path)."""
-
-    def __init__(self, index, rank: int, world: int, device: int):
-        import torch
-
-        from . import _core
-
-        self.core = _core
-        self.index = index
-        self.rank, self.world, self.device = rank, world, device
-        self.torch = torch
-
-    def step(self, d_words, n_queries: int, query_planes: int, geometry, n: int, variant: str = "auto"):
-        """One batch: local scan + select into a device tensor, NCCL gather,
-        GPU merge on rank 0.  Returns (merged uint8 tensor [Q*n*32] on rank 0
-        else None, local stats)."""
-        torch = self.torch
-        stream = torch.cuda.current_stream(self.device)
-        out = torch.empty(n_queries * n * RESULT_BYTES, dtype=torch.uint8, device=f"cuda:{self.device}")
-        stats = self.core.search_device(self.index.handle(0), d_words.data_ptr(), n_queries, query_planes, geometry,
-                                        n, out.data_ptr(), stream.cuda_stream, variant)
-
-        def merge(blocks):
-            if len(blocks) == 1:
-                return blocks[0]
-            cat = torch.cat(blocks)
-            merged = torch.empty_like(blocks[0])
-            self.core.merge_device(self.device, cat.data_ptr(), len(blocks), n_queries, n, merged.data_ptr(),
-                                   stream.cuda_stream)
-            return merged
-
-        merged = gather_and_merge(out, self.rank, self.world, merge)
-        return merged, stats
-
-
-def decode_results(buf, n_queries: int, n: int):
-    """uint8 [Q*n*32] (rbe_result records) -> list of [(score, id, partition)]."""
-    import numpy as np
-
-    raw = buf.cpu().numpy() if hasattr(buf, "cpu") else np.asarray(buf)
-    rec = np.frombuffer(raw.tobytes(), dtype=np.dtype([("score", "<f8"), ("id", "<u8"), ("acc", "<i8"),
-                                                       ("partition", "<u4"), ("valid", "<u4")]))
-    rec = rec.reshape(n_queries, n)
-    out = []
-    for q in range(n_queries):
-        row = []
-        for r in rec[q]:
-            if not r["valid"]:
-                break
-            row.append((float(r["score"]), int(r["id"]), int(r["partition"])))
-        out.append(row)
-    return out
