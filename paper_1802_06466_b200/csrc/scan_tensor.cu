@@ -739,11 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 const float* msrc = part.mags + si.base;
                 const uint64_t tile_words = uint64_t(p.tpb) * w32;
                 for (uint32_t i = 0; i < si.n_tiles; ++i, rs.next(nst)) {
-#ifdef RBE_EXP_PRODUCER_BACKOFF
-                    mbar_wait_backoff(empty + rs.idx, rs.phase ^ 1);
-#else
                     mbar_wait(empty + rs.idx, rs.phase ^ 1);
-#endif
                     mbar_expect_tx(full + rs.idx, stage_bytes);
                     uint8_t* dst = ring + rs.idx * stage_bytes;
 #pragma unroll
@@ -929,11 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                     RBE_CLK(c0);
                     if (has_next) {
                         seek(k_n >> spt_sh);
-#ifdef RBE_EXP_FULL_NAP
-                        mbar_wait_nap(full + st_idx, st_ph);
-#else
                         mbar_wait(full + st_idx, st_ph);
-#endif
                         RBE_CLK(c0b);
                         RBE_ACC(0, c0b - c0);
                         expand(st_idx, (k_n & (spt - 1)) * 128 + l, (kc + 1) & 1, mag_n);
@@ -1517,7 +1509,7 @@ TensorScanPlan plan_tensor_scan(const Shape& s, uint32_t qp, const rbe_scan_geom
     pl.Q = Q;
     pl.qp = qp;
     pl.n = n;
-    pl.probe_tiles = probe_tiles ? probe_tiles : 8;
+    pl.probe_tiles = probe_tiles ? probe_tiles : 4;  // 4 of 256 tiles per strip (tools/probe_tiles_sweep.py)
     pl.prefix.assign(counts.size() + 1, 0);
     const uint64_t threads = uint64_t(g.blocks) * g.threads_per_block;
     uint64_t total = 0;
