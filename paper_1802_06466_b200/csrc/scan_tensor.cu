@@ -1434,12 +1434,11 @@ uint32_t pick_nwg(uint32_t w32) {
     return 0;
 }
 
-// ring depth: as many stages (<= kStages) as shared memory allows
-uint32_t pick_stages(uint32_t kp, uint32_t w32, uint32_t sw) {
+// ring depth: as many stages (<= kStages) as shared memory allows (the probe keeps two state
+// tables, so its ring is shallower)
+uint32_t pick_stages(uint32_t kp, uint32_t w32, uint32_t sw, bool probe) {
     for (uint32_t ns = kStages; ns >= 2; --ns)
-        if (smem_layout(kp, w32, kQPass, ns, sw, false).total <= kSmemLimit &&
-            smem_layout(kp, w32, kQPass, ns, sw, true).total <= kSmemLimit)
-            return ns;
+        if (smem_layout(kp, w32, kQPass, ns, sw, probe).total <= kSmemLimit) return ns;
     return 0;
 }
 
@@ -1492,7 +1491,8 @@ bool tensor_supported(const Shape& s, uint32_t qp, const rbe_scan_geometry& g, u
     if (s.wpp > 4) return no("dim > 256");
     if (Q == 0) return no("no queries");
     if (!pick_nwg(s.w32)) return no("tensor memory");
-    if (pick_stages(s.kp, s.w32, strip_width(g)) == 0) return no("shared memory");
+    if (pick_stages(s.kp, s.w32, strip_width(g), true) == 0 || pick_stages(s.kp, s.w32, strip_width(g), false) == 0)
+        return no("shared memory");
     if (pick_lam_shift(s, qp) < 0) return no("accumulator range exceeds the threshold block");
     if (g.items_per_thread >= 511) return no("items_per_thread >= 511 (state key)");
     if (uint64_t(g.items_per_thread) * g.threads_per_block >= (1ull << 31)) return no("logical block span >= 2^31 slots");
@@ -1586,7 +1586,6 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
         const uint64_t dmax = (2ull << lam_shift) * vmax * (64ull * s.wpp) * rqmax;
         tp.f16max = dmax < 32767 ? int32_t(dmax) : 0;
     }
-    tp.nstages = pick_stages(s.kp, s.w32, tp.sw);
     tp.ptop = plan.ptop;
     tp.n_pad = n_pad;
     tp.L = s.rw ? (a.qp + s.kp - 2) : 0;
@@ -1632,7 +1631,8 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
             // probe: a warpgroup's lanes must always hold the same logical threads (nwg = spt)
             TensorParams pp = tp;
             if (tp.sw > 128 && tp.nwg % 2) pp.nwg = 2;  // nwg a multiple of spt (4 stays)
-            dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, true).total, grid, st);
+            pp.nstages = pick_stages(s.kp, s.w32, tp.sw, true);
+            dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, pp.nstages, tp.sw, true).total, grid, st);
         }
         const size_t tsm = size_t(kThetaCap) * 4;
         RBE_CK(cudaFuncSetAttribute(theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsm)));
@@ -1645,6 +1645,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
             RBE_CK(cudaMemsetAsync(d_prof, 0, sizeof(unsigned long long) * 2048 * 16 * 8, st));
             tp.prof = d_prof;
         }
+        tp.nstages = pick_stages(s.kp, s.w32, tp.sw, false);
         dispatch<false>(s.kp, s.rw != 0, tp, smem_layout(s.kp, s.w32, n_pad, tp.nstages, tp.sw, false).total, grid, st);
         tp.prof = nullptr;
         if (prof) {
