@@ -87,6 +87,17 @@ constexpr int kBins = 64;            // dynamic-theta histogram bins per query
 constexpr int kHiCols = 24;          // X block: K bytes 8..31 hold 255 (the c_q "high" part)
 constexpr int32_t kXMax = 255 * kHiCols * 127 + 127;  // largest |X| the block can encode
 constexpr int32_t kEMax = 4 * 127;   // e_q is split over 4 K bytes
+#ifndef RBE_CC_MAXQ
+#define RBE_CC_MAXQ 2
+#endif
+// Small batches (<= kCCMaxQ live queries, dim 128, <= 7 keyword planes): the same kernel scores
+// each (doc, query) on the CUDA cores (__dp4a of the expanded doc bytes with the query operand
+// rows, plus X_q(j)) instead of the tensor core -- exactly the F the MMA would produce, so the
+// candidate sets, the selection and the results are the same; no MMA chain or TMEM round trip
+// per sub-tile (the latency path of SURVEY.md C4).
+constexpr uint32_t kCCMaxQ = RBE_CC_MAXQ;
+constexpr uint32_t kCCUnroll = 8;    // query loop bound of the CUDA-core body (>= kCCMaxQ)
+static_assert(kCCMaxQ <= kCCUnroll, "CUDA-core batch bound");
 
 struct TensorParams {
     const PartDesc* parts;
@@ -622,7 +633,7 @@ __device__ __noinline__ void emit_pair(const TensorParams& p, int32_t F, uint32_
 
 // W = 4: the common shape fixed at compile time -- dim 128 (w32 = 4), 256-doc strips, three
 // worker warpgroups (two in the probe); W = 0: every shape from TensorParams
-template <int KP, bool RW, bool PROBE, int W>
+template <int KP, bool RW, bool PROBE, int W, bool CC = false>
 __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr bool kFixed = W == 4;
@@ -902,7 +913,73 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             }
             xpar = sidx & 1;
             uint32_t k = (wg + nwg - u0 % nwg) % nwg;
-            if (k < n_sub) {
+            if constexpr (CC) {
+                // ---- CUDA-core body: thread l scores doc l of each of this warpgroup's sub-tiles
+                static_assert(W == 4 && KP <= 7, "CUDA-core body: dim 128, u8 doc bytes <= 127 (__dp4a s8)");
+                const int32_t* xc = xcoef + xpar * 3 * kQPass;
+                const float pscale = PROBE ? ldexpf(1.0f, -L - int(p.lam_shift)) : 0.0f;
+                for (; k < n_sub; k += nwg) {
+                    const uint32_t ti = k >> spt_sh, t_abs = tiles0 + ti;
+                    const uint32_t st_idx = t_abs % nst, st_ph = (t_abs / nst) & 1;
+                    const uint32_t col = (k & (spt - 1)) * 128 + l;
+                    mbar_wait(full + st_idx, st_ph);
+                    const uint8_t* stage = ring + st_idx * stage_bytes;
+                    const uint4* src = reinterpret_cast<const uint4*>(stage) + col;
+                    uint32_t w0[KP], w1[KP], w2[KP], w3[KP];
+#pragma unroll
+                    for (int t = 0; t < KP; ++t) {
+                        const uint4 v = src[t * sw];
+                        w0[t] = v.x;
+                        w1[t] = v.y;
+                        w2[t] = v.z;
+                        w3[t] = v.w;
+                    }
+                    const float mag = reinterpret_cast<const float*>(stage + KP * plane_bytes)[col];
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + st_idx);
+                    uint32_t V[32];  // doc bytes of K [4i, 4i + 4) in V[i] (the A row of the MMA)
+                    ExpandStored<KP, RW>::run(w0, V);
+                    ExpandStored<KP, RW>::run(w1, V + 8);
+                    ExpandStored<KP, RW>::run(w2, V + 16);
+                    ExpandStored<KP, RW>::run(w3, V + 24);
+                    const int32_t j = int32_t(mag_bin(mag, p.m0f, p.inv_df));
+                    const bool valid = ti * p.tpb + col < lim;
+                    const float scale = PROBE ? __fdiv_rn(pscale, mag) : 0.0f;
+#pragma unroll
+                    for (uint32_t q = 0; q < kCCUnroll; ++q) {
+                        if (q >= p.nq) break;
+                        // F = sum_K V x B_q + X_q(j), B row q of the query operand (core-matrix layout)
+                        int32_t F = xc[q] - xc[kQPass + q] * j - xc[2 * kQPass + q] * (j >> 4);
+                        const uint8_t* brow = bsm + (q / 8) * 256 + (q % 8) * 16;
+#pragma unroll
+                        for (int c16 = 0; c16 < 8; ++c16) {
+                            const uint4 b = *reinterpret_cast<const uint4*>(brow + (c16 >> 1) * (p.n_pad * 32) +
+                                                                            (c16 & 1) * 128);
+                            F = __dp4a(int(V[4 * c16 + 0]), int(b.x), F);
+                            F = __dp4a(int(V[4 * c16 + 1]), int(b.y), F);
+                            F = __dp4a(int(V[4 * c16 + 2]), int(b.z), F);
+                            F = __dp4a(int(V[4 * c16 + 3]), int(b.w), F);
+                        }
+                        if (PROBE) {
+                            if (valid) pm[q] = fmaxf(pm[q], float(F) * scale);
+                        } else if (F >= 0 && valid) {
+                            ++cands;
+                            const uint32_t pos = atomicAdd(cq_count, 1u);
+                            if (pos < kCandQueue)
+                                cqueue[pos] = make_uint2((q << 26) | ti, (col << 24) | uint32_t(F));
+                            else {
+                                const StripInfo si = strip_info(p, s);
+                                if (p.lossless)
+                                    emit_pair(p, F, q, ti, col, p.parts[si.part], si.base, xc, cq_s[q], theta_s);
+                                else
+                                    take_pair(F, q, ti, col, p.parts[si.part].mags + si.base + col, xc, cq_s[q],
+                                              p.m0f, p.inv_df, p.lam_shift, p.error, sw, theta_s, st_key, p.tpb, L,
+                                              touched, tcount);
+                            }
+                        }
+                    }
+                }
+            } else if (k < n_sub) {
                 // ring position of sub-tile k's stage; advanced incrementally (at most a few stages per step)
                 uint32_t ti = k >> spt_sh;
                 uint32_t st_idx = (tiles0 + ti) % nst, st_ph = ((tiles0 + ti) / nst) & 1;
@@ -1395,10 +1472,16 @@ uint64_t count_strips(const rbe_scan_geometry& g, uint64_t count) {
     return blocks * (g.threads_per_block / strip_width(g));
 }
 
+bool cc_body(const TensorParams& tp, uint32_t kp) {
+    return tp.w32 == 4 && tp.sw == 256 && tp.nwg == 4u && kp <= 7 && tp.nq <= kCCMaxQ;
+}
+
 template <int KP, bool RW, bool PROBE>
 void launch_kernel(const TensorParams& tp, size_t smem, int grid, cudaStream_t st) {
     const bool fixed = tp.w32 == 4 && tp.sw == 256 && tp.nwg == 4u;
     auto k = fixed ? tensor_scan_kernel<KP, RW, PROBE, 4> : tensor_scan_kernel<KP, RW, PROBE, 0>;
+    if constexpr (KP <= 7)
+        if (cc_body(tp, KP)) k = tensor_scan_kernel<KP, RW, PROBE, 4, true>;
     RBE_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k<<<grid, kThreads, smem, st>>>(tp);
     RBE_CK(cudaGetLastError());

@@ -236,6 +236,48 @@ def test_tensor_matches_reference(rbe, port, case):
     check_accs(got, accs, mags_by_id(parts), qp, kp, rw)
 
 
+SMALL_BATCH = [
+    # N, kp, qp, P, geometry, n, rw, Q -- dim 128, 256-wide strips: <= 2 live queries take the
+    # CUDA-core scoring body of the tensor scan (kCCMaxQ, scan_tensor.cu)
+    (200000, 3, 3, 1, (4, 256, 256, 1), 100, True, 1),
+    (200000, 3, 3, 1, (4, 256, 256, 1), 1000, True, 2),
+    (150000, 1, 3, 3, (2, 256, 128, 1), 50, True, 2),
+    (150000, 2, 2, 2, (1, 512, 256, 1), 200, True, 1),
+    (150000, 4, 3, 1, (3, 256, 256, 1), 100, False, 2),
+    (100000, 7, 2, 1, (2, 256, 256, 1), 300, True, 1),
+    (100000, 3, 3, 2, (2, 256, 256, 256), 500, True, 2),   # lossless (queue_length >= items_per_thread)
+]
+
+
+@pytest.mark.parametrize("case", SMALL_BATCH)
+def test_small_batch_matches_reference(rbe, port, case):
+    """Batches of one or two queries (the latency path): the CUDA-core scoring body computes the
+    same F as the tensor core, so results equal the reference bit for bit."""
+    N, kp, qp, P, geo, n, rw, Q = case
+    ref = Ref()
+    parts = synthetic_partitions(31, N, 128, kp, P, rw, port)
+    qs = gen_queries(37, Q, 128, qp)
+    want, scored = ref.index(128, kp, rw, parts).search(qs, geo, n, threads=8)
+    dix = device_index(rbe, 128, kp, rw, parts)
+    got, accs, counts, stats = gpu_search(rbe, dix, qs, geo, n, "tensor")
+    assert stats["scored"] == scored == Q * N
+    assert got == want, case
+    check_accs(got, accs, mags_by_id(parts), qp, kp, rw)
+
+
+def test_small_batch_matches_exact_at_scale(rbe):
+    """8M docs, 1 and 2 queries: the CUDA-core body of the tensor scan == the exact kernel."""
+    N = 8_000_000
+    geo = (-(-N // 65536), 256, 256, 1)
+    dix = rbe.DeviceIndex.synthetic(128, 3, True, N, 1, 0xD0C5)
+    for Q in (1, 2):
+        qs = gen_queries(0x0E1 + Q, Q, 128, 3)
+        a = gpu_search(rbe, dix, qs, geo, 1000, "exact")
+        b = gpu_search(rbe, dix, qs, geo, 1000, "auto")
+        assert a[0] == b[0]
+        assert np.array_equal(a[1], b[1])
+
+
 def test_tensor_state_table_overflow(rbe, port):
     """n above the survivor count (theta stays -inf): every (query, logical thread)
     state entry of a strip is set -- 40 queries x 256 threads > the 4096-entry

@@ -27,7 +27,7 @@ def build(tag, flags):
     print("built", tag)
 
 
-def time_variant(tag, n):
+def time_variant(tag, n, Q=64):
     sys.path.insert(0, os.path.join(ROOT, "exp_libs", tag) if tag != "head" else ROOT)
     sys.path.insert(1, ROOT)
     import paper_1802_06466_b200 as rbe
@@ -35,7 +35,7 @@ def time_variant(tag, n):
     dix = rbe.DeviceIndex.synthetic(128, 3, True, n, 1, 0xD0C5, [0])
     g = rbe.ScanGeometry()
     g.blocks = -(-n // 65536)
-    qs = gen_queries(0x0E1, 64, 128, 3)
+    qs = gen_queries(0x0E1, Q, 128, 3)
     ref = None
     for _ in range(2):
         ref = dix.search_words(qs, g, 1000)
@@ -45,12 +45,13 @@ def time_variant(tag, n):
     ms = sorted(t[5]["device_ms"] for t in ts)
     import hashlib
     h = hashlib.sha256(b"".join(a.tobytes() for a in ref[:5])).hexdigest()[:16]
-    print(f"[{tag}] n={n} device_ms best {ms[0]:.4f} median {ms[3]:.4f} cands {ts[0][5].get('candidates')} sha {h}")
+    print(f"[{tag}] n={n} Q={Q} device_ms best {ms[0]:.4f} median {ms[3]:.4f} cands {ts[0][5].get('candidates')} sha {h}")
     return ref
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "--time":
-        time_variant(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 100_000_000)
+        time_variant(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 100_000_000,
+                     int(sys.argv[4]) if len(sys.argv) > 4 else 64)
     else:
         build(sys.argv[1], sys.argv[2:])
