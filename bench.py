@@ -407,7 +407,7 @@ def run_ours(args):
     sweep = None
     if world == 1 and has_docs and not args.no_q_sweep:
         sweep = []
-        for nq in (1, 8, 16, 64, 128, 256):
+        for nq in (1, 2, 8, 16, 64, 128, 256):
             qw = gen_queries(SEED_QUERIES + nq, nq, DIM, QP)
             dw = torch.from_numpy(qw.view(np.int64).copy()).to(dev)
             ob = torch.empty(nq * K * RESULT_BYTES, dtype=torch.uint8, device=dev)

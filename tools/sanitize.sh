@@ -1,6 +1,6 @@
 #!/bin/bash
 # Run under gpurun: compute-sanitizer memcheck / racecheck / synccheck over smoke()
-# (tensor + exact scan, probe, theta, select on 40K docs) and the device merge test.
+# (exact scan, tensor scan with its tensor-core and CUDA-core bodies, probe, theta, select on 40K docs) and the device merge test.
 # Logs: gpurun_out/sanitizer_<tool>.log
 for tool in memcheck racecheck synccheck; do
   timeout -s KILL 900 compute-sanitizer --tool $tool --print-limit 50 \
