@@ -121,7 +121,7 @@ struct TensorParams {
     const int32_t* cq;             // [Q] query constants
     const double* theta;           // [Q] exact-score threshold (main pass)
     uint32_t probe_tiles;          // probe pass: tiles per strip (0 = main pass)
-    float* probe_out;              // [Q][n_strips][ptop]
+    float* probe_out;              // [Q][n_strips][ptop] (probe launch: n_strips = the probed strips)
     uint64_t n_strips;
     Result* surv;
     unsigned long long* surv_count;
@@ -903,12 +903,13 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 const uint64_t lim64 = count > si.base ? count - si.base : 0;
                 lim = uint32_t(lim64 < 0xffffffffull ? lim64 : 0xffffffffull);
                 if (wt == 0 && !PROBE) {
-                    unsigned long long valid_docs = 0;
-                    for (uint32_t t = 0; t < n_tiles; ++t) {
-                        const uint64_t o = uint64_t(t) * p.tpb;
-                        valid_docs += o < lim64 ? (lim64 - o < sw ? lim64 - o : sw) : 0;
-                    }
-                    atomicAdd(p.scored, valid_docs * p.nq);
+                    // valid docs = sum over tiles t < n_tiles of clamp(lim64 - t tpb, 0, sw), closed form
+                    // (sw divides tpb): f full tiles, then at most one partial one
+                    const uint64_t f =
+                        lim64 >= sw ? std::min<uint64_t>(n_tiles, (lim64 - sw) / p.tpb + 1) : 0;
+                    uint64_t valid_docs = f * sw;
+                    if (f < n_tiles && lim64 > f * p.tpb) valid_docs += std::min<uint64_t>(lim64 - f * p.tpb, sw);
+                    atomicAdd(p.scored, (unsigned long long)(valid_docs * p.nq));
                 }
             }
             xpar = sidx & 1;
@@ -1645,7 +1646,10 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
                                                      uint32_t(lam_shift), bimg, cq);
     RBE_CK(cudaGetLastError());
     uint32_t launches = 1;
-    const uint64_t per_query = n_strips * plan.ptop;
+    // theta_kernel reads the first kThetaCap probe values of a query (any subset of distinct
+    // threads bounds the n-th survivor): the probe runs only over the strips that feed them
+    const uint64_t probe_strips = std::min<uint64_t>(n_strips, kThetaCap / plan.ptop);
+    const uint64_t per_query = probe_strips * plan.ptop;  // probe_out: [Q][probe_strips][ptop]
     float* probe = static_cast<float*>(d_probe);
 
     // magnitude bins: m0 + Delta j <= m for j = floor((m - m0)/Delta - 1e-3) in [0, 255]
@@ -1715,6 +1719,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
             TensorParams pp = tp;
             if (tp.sw > 128 && tp.nwg % 2) pp.nwg = 2;  // nwg a multiple of spt (4 stays)
             pp.nstages = pick_stages(s.kp, s.w32, tp.sw, true);
+            pp.n_strips = probe_strips;
             dispatch<true>(s.kp, s.rw != 0, pp, smem_layout(s.kp, s.w32, n_pad, pp.nstages, tp.sw, true).total, grid, st);
         }
         const size_t tsm = size_t(kThetaCap) * 4;
