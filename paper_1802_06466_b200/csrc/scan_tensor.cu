@@ -1202,53 +1202,27 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             named_bar(kAllBar, n_workers);
             if (wt == 0) *cq_count = 0;
             // emit the strip's survivors >= theta (one per (query, logical thread)) from the
-            // list of state entries set in this strip: pass 1 counts per query, one global
-            // reservation per query, pass 2 writes; the histogram is merged in shared memory
+            // list of state entries set in this strip, each with its own slot reservation in the
+            // query's survivor list (one pass: the list order is irrelevant, global_select sorts);
+            // the histogram is merged in shared memory
             {
-                uint32_t* scnt = reinterpret_cast<uint32_t*>(cqueue);                             // [64]
-                unsigned long long* sbase = reinterpret_cast<unsigned long long*>(scnt + kQPass);  // [64]
-                uint32_t* hist_s = reinterpret_cast<uint32_t*>(sbase + kQPass);                    // [64][kBins]
+                uint32_t* hist_s = reinterpret_cast<uint32_t*>(cqueue);  // [64][kBins]
                 // entries to visit: the touched list, or the whole table when it overflowed
                 const bool scan_all = *tcount > kTouchedCap;
                 const uint32_t nt = scan_all ? kQPass * sw : *tcount;
-                if (wt < kQPass) scnt[wt] = 0;
                 for (uint32_t k2 = wt; k2 < kQPass * kBins; k2 += n_workers) hist_s[k2] = 0;
                 named_bar(kAllBar, n_workers);
-                auto survivor = [&](uint32_t ent, uint32_t& q, uint64_t& slot, int32_t& a, double& sc) {
+                for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
+                    const uint32_t ent = scan_all ? k2 : touched[k2];
                     const uint32_t key = st_key[ent];
-                    q = ent / sw;
-                    const uint32_t cc = ent % sw;
-                    a = key_acc(key);
-                    slot = si.base + cc + uint64_t(key_i(key)) * p.tpb;
-                    sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
-                    return sc >= theta_s[q];  // theta may have risen since the entry was set
-                };
-                for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
-                    const uint32_t ent = scan_all ? k2 : touched[k2];
-                    if (scan_all && st_key[ent] == kEmptyKey) continue;
-                    uint32_t q;
-                    uint64_t slot;
-                    int32_t a;
-                    double sc;
-                    if (survivor(ent, q, slot, a, sc)) atomicAdd(scnt + q, 1u);
-                }
-                named_bar(kAllBar, n_workers);
-                if (wt < p.nq) {
-                    sbase[wt] = scnt[wt] ? atomicAdd(p.surv_count + p.q0 + wt, (unsigned long long)scnt[wt]) : 0ull;
-                    scnt[wt] = 0;
-                }
-                named_bar(kAllBar, n_workers);
-                for (uint32_t k2 = wt; k2 < nt; k2 += n_workers) {
-                    const uint32_t ent = scan_all ? k2 : touched[k2];
-                    if (scan_all && st_key[ent] == kEmptyKey) continue;
-                    uint32_t q;
-                    uint64_t slot;
-                    int32_t a;
-                    double sc;
-                    const bool keep = survivor(ent, q, slot, a, sc);
+                    if (key == kEmptyKey) continue;
                     st_key[ent] = kEmptyKey;
-                    if (!keep) continue;
-                    const unsigned long long pos = sbase[q] + atomicAdd(scnt + q, 1u);
+                    const uint32_t q = ent / sw, cc = ent % sw;
+                    const int32_t a = key_acc(key);
+                    const uint64_t slot = si.base + cc + uint64_t(key_i(key)) * p.tpb;
+                    const double sc = __ddiv_rn(ldexp(double(a), -L), double(__ldg(part.mags + slot)));
+                    if (!(sc >= theta_s[q])) continue;  // theta may have risen since the entry was set
+                    const unsigned long long pos = atomicAdd(p.surv_count + p.q0 + q, 1ull);
                     if (pos < p.surv_cap) {
                         Result r;
                         r.score = sc;
