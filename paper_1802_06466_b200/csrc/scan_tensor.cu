@@ -194,7 +194,7 @@ __device__ __forceinline__ void mbar_wait_nap(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     while (!ok) {
-        __nanosleep(64);
+        __nanosleep(64);  // 24 ns measured the same
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -498,7 +498,7 @@ struct RingPos {
 };
 
 struct SmemLayout {
-    size_t b, xb, state, cqueue, touched, qconst, bars, ax, total;
+    size_t desc, ring, b, xb, state, cqueue, touched, qconst, bars, ax, total;
 };
 
 __host__ __device__ inline size_t stage_bytes_of(uint32_t kp, uint32_t w32, uint32_t sw) {
@@ -509,7 +509,10 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t kp, uint32_t w32, uin
                                                   uint32_t sw, bool probe) {
     auto al = [](size_t x) { return (x + 127) & ~size_t(127); };
     SmemLayout s{};
-    size_t off = al(size_t(nstages) * stage_bytes_of(kp, w32, sw));
+    s.desc = 0;  // MMA operand table: [kMaxWG][2 A buffers][2 X parities] x 32 B, at a fixed offset
+    const size_t ring = al(kMaxWG * 2 * 2 * 32);
+    s.ring = ring;
+    size_t off = al(ring + size_t(nstages) * stage_bytes_of(kp, w32, sw));
     s.b = off;  // data K blocks of the query operand
     off = al(off + size_t(n_pad) * 32 * w32);
     s.xb = off;  // two X blocks (threshold), indexed by strip parity
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     const uint32_t plane_bytes = sw * w32 * 4;               // one plane of a stage (sw docs)
     const uint32_t stage_bytes = KP * plane_bytes + sw * 4;  // + the stage's f32 magnitudes
     SmemLayout sl = smem_layout(KP, w32, p.n_pad, nst, sw, PROBE);
-    uint8_t* ring = smem;
+    uint8_t* ring = smem + sl.ring;
     uint8_t* bsm = smem + sl.b;
     uint8_t* xsm = smem + sl.xb;  // [2][n_pad * 32]
     uint32_t* st_key = reinterpret_cast<uint32_t*>(smem + sl.state);  // [64][sw]
@@ -735,6 +738,19 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // MMA operands of (warpgroup w, A buffer ab, X parity xp), built once: the issuing warp reads
+    // 32 bytes instead of rebuilding descriptors on the critical path of every group
+    uint4* desc_tab = reinterpret_cast<uint4*>(smem);  // sl.desc == 0
+    if (threadIdx.x < kMaxWG * 4) {
+        const uint32_t w = threadIdx.x >> 2, ab = (threadIdx.x >> 1) & 1, xp = threadIdx.x & 1;
+        const uint64_t b0 = smem_desc(smem_u32(bsm));
+        const uint64_t xd = smem_desc(smem_u32(xsm) + xp * p.n_pad * 32);
+        const uint64_t axd = smem_desc_lbo(smem_u32(axs) + (w * 2 + ab) * kXTile, (2 * kMaxWG - (w * 2 + ab)) * kXTile, 128);
+        const uint32_t a_w = tmem_base + w * wg_cols;
+        desc_tab[2 * threadIdx.x] = make_uint4(uint32_t(b0), uint32_t(b0 >> 32), uint32_t(xd), uint32_t(xd >> 32));
+        desc_tab[2 * threadIdx.x + 1] = make_uint4(uint32_t(axd), uint32_t(axd >> 32), a_w + ab * a_cols, a_w + 2 * a_cols);
+    }
+    __syncthreads();
 
     if (warp == kProducerWarp) {
         // ===================== producer: one contiguous sw-doc stage per tile of each strip =====================
@@ -853,7 +869,6 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
         // This warp's part of A(k) is complete and its reads of D are done.  The last of the
         // warpgroup's eight warps to get here issues MMA(k) (whole warp, one elected lane), so no
         // warp ever waits for an issuer: the per-warpgroup counter in shared memory orders it.
-        const uint32_t a_w = tmem_base + wg * wg_cols;  // lane 0 of this warpgroup's A[0]
         uint32_t xpar = 0;  // X block parity of the current strip
         auto arrive_a = [&](uint32_t ab) {
             tmem_wait_st();
@@ -869,15 +884,14 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             old = __shfl_sync(0xffffffffu, old, 0);
             if ((old & uint32_t(kWGWarps - 1)) == uint32_t(kWGWarps - 1)) {
                 tc_fence_after();
-                // descriptors rebuilt here (cheap, uniform) rather than held across the loop
                 const uint32_t idesc = idesc_i8(128, p.n_pad);
-                const uint64_t b_desc0 = smem_desc(opaque_u32(smem_u32(bsm)));
                 const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
-                const uint64_t xd = smem_desc(opaque_u32(smem_u32(xsm) + xpar * p.n_pad * 32));
-                const uint32_t a_t = a_w + ab * a_cols;
-                const uint32_t d_w = a_w + 2 * a_cols;
-                const uint32_t ax_addr = opaque_u32(smem_u32(axs)) + (wg * 2 + ab) * kXTile;
-                const uint64_t ax_desc = smem_desc_lbo(ax_addr, (2 * kMaxWG - (wg * 2 + ab)) * kXTile, 128);
+                const uint4* e = desc_tab + 2 * (((wg * 2 + ab) * 2) + xpar);
+                const uint4 e0 = e[0], e1 = e[1];
+                const uint64_t b_desc0 = uint64_t(e0.x) | (uint64_t(e0.y) << 32);
+                const uint64_t xd = uint64_t(e0.z) | (uint64_t(e0.w) << 32);
+                const uint64_t ax_desc = uint64_t(e1.x) | (uint64_t(e1.y) << 32);
+                const uint32_t a_t = e1.z, d_w = e1.w;
                 switch (w32) {
                     case 2: mma_group<2>(d_w, a_t, b_desc0, b_step, ax_desc, xd, idesc); break;
                     case 4: mma_group<4>(d_w, a_t, b_desc0, b_step, ax_desc, xd, idesc); break;
