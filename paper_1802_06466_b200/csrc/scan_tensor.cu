@@ -927,6 +927,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                 }
             }
             xpar = sidx & 1;
+            // packed-epilogue flag of this strip's X block (fixed for the strip): read once, not
+            // on every sub-tile's path from the MMA wait to the accumulator load
+            const bool p16 = p16ok[xpar] != 0;
             uint32_t k = (wg + nwg - u0 % nwg) % nwg;
             if constexpr (CC) {
                 // ---- CUDA-core body: thread l scores doc l of each of this warpgroup's sub-tiles
@@ -1046,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                         // F >= 0 is necessary for score >= theta: AND the sign bits per group of 8
                         constexpr int kG = kQH / 8;  // groups of 8 queries per warp
                         uint32_t gmask = 0;  // bit g: some F >= 0 among queries qh + [8g, 8g+8)
-                        if (p16ok[xpar] != 0) {
+                        if (p16) {
                             // low 16 bits of the warp's accumulators, two per register (pack::16b); the
                             // sign of every F >= 0 survives, a wrapped F < 0 is rejected exactly below
                             uint32_t R[kQH / 2];
@@ -1080,8 +1083,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
                             if (!valid) gmask = 0;
                         }
                         // groups with a passing pair in any lane (tcgen05.ld is warp-collective)
-                        uint32_t wmask = __reduce_or_sync(0xffffffffu, gmask);
-                        if (wmask) {
+                        // a vote first (short latency; candidates are rare), the OR of the masks only then
+                        if (__any_sync(0xffffffffu, gmask != 0u)) {
+                            uint32_t wmask = __reduce_or_sync(0xffffffffu, gmask);
                             do {
                                 const uint32_t g = uint32_t(__ffs(wmask) - 1);
                                 wmask &= wmask - 1;
