@@ -884,8 +884,9 @@ __global__ void __launch_bounds__(kThreads, 1) tensor_scan_kernel(TensorParams p
             old = __shfl_sync(0xffffffffu, old, 0);
             if ((old & uint32_t(kWGWarps - 1)) == uint32_t(kWGWarps - 1)) {
                 tc_fence_after();
-                const uint32_t idesc = idesc_i8(128, p.n_pad);
-                const uint64_t b_step = uint64_t(p.n_pad * 32) >> 4;  // K block stride in descriptor units
+                // MMA N = 64 (run_tensor_scan always pads a pass to kQPass queries): compile-time
+                constexpr uint32_t idesc = idesc_i8(128, kQPass);
+                constexpr uint64_t b_step = uint64_t(kQPass * 32) >> 4;  // K block stride in descriptor units
                 const uint4* e = desc_tab + 2 * (((wg * 2 + ab) * 2) + xpar);
                 const uint4 e0 = e[0], e1 = e[1];
                 const uint64_t b_desc0 = uint64_t(e0.x) | (uint64_t(e0.y) << 32);
@@ -1621,7 +1622,7 @@ uint32_t run_tensor_scan(const TensorScanPlan& plan, const ScanArgs& a, const Sh
     RBE_CK(cudaMemcpyAsync(d_prefix, plan.prefix.data(), sizeof(uint64_t) * plan.prefix.size(), cudaMemcpyHostToDevice,
                            st));
     const uint32_t passes = (Q + kQPass - 1) / kQPass;
-    const uint32_t n_pad = kQPass;
+    const uint32_t n_pad = kQPass;  // the kernel's MMA issue assumes N = kQPass
     const int lam_shift = pick_lam_shift(s, a.qp);
     if (lam_shift < 0) throw std::invalid_argument("tensor scan: accumulator range exceeds the threshold block");
     uint8_t* bimg = static_cast<uint8_t*>(d_qtensor);
