@@ -88,7 +88,7 @@ constexpr int kHiCols = 24;          // X block: K bytes 8..31 hold 255 (the c_q
 constexpr int32_t kXMax = 255 * kHiCols * 127 + 127;  // largest |X| the block can encode
 constexpr int32_t kEMax = 4 * 127;   // e_q is split over 4 K bytes
 #ifndef RBE_CC_MAXQ
-#define RBE_CC_MAXQ 2
+#define RBE_CC_MAXQ 1
 #endif
 // Small batches (<= kCCMaxQ live queries, dim 128, <= 7 keyword planes): the same kernel scores
 // each (doc, query) on the CUDA cores (__dp4a of the expanded doc bytes with the query operand
